@@ -1,0 +1,170 @@
+/*
+ * mixtile_b200 -- C ABI of the B200-native mixed-precision tile-Cholesky
+ * Gaussian log-likelihood (arXiv 2003.05324), drop-in for the reference
+ * package `mixtile`'s hot path.
+ *
+ * Every entry point takes plain pointers and sizes.  Device pointers are
+ * allocated by the caller (the Python host uses torch's caching allocator);
+ * `stream` is a cudaStream_t passed as void*.  All calls are asynchronous on
+ * `stream` unless documented otherwise; `mt_read_status` synchronises.
+ * Return value: MT_OK, or an MT_E* code with details in mt_last_error().
+ *
+ * The reference interfaces each entry replaces (paths under the reference's
+ * pkg/src/mixtile/) are cited per function.
+ */
+#ifndef MIXTILE_B200_H
+#define MIXTILE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: map 1:1 onto the reference's exception types */
+#define MT_OK 0
+#define MT_E_NOT_SPD 1      /* factor.FactorizationError(index)       factor.py:31-37  */
+#define MT_E_OVERFLOW 2     /* tilestore.PrecisionOverflowError       tilestore.py:20  */
+#define MT_E_BAD_ARG 3      /* ValueError                                               */
+#define MT_E_CUDA 4         /* RuntimeError (CUDA/NCCL failure)                         */
+
+/* precision modes (tilestore.Mode, tilestore.py:24-27) */
+#define MT_MODE_DP 0
+#define MT_MODE_MP 1
+#define MT_MODE_DST 2
+
+/* distance metrics (covmath.DistanceMetric, covmath.py:299-317) */
+#define MT_METRIC_EUCLIDEAN 0
+#define MT_METRIC_GREAT_CIRCLE 1
+
+/*
+ * Device-resident lower tile grid of an n x n symmetric matrix
+ * (replaces tilestore.TileMatrix, tilestore.py:139-205).
+ *
+ * Tiles are nb x nb, ROW-major, padded: the last tile row/column is padded
+ * to nb with identity on the diagonal and zeros elsewhere, which leaves the
+ * factor, logdet and solves of the n x n problem unchanged.  Tile (i,j),
+ * i >= j, is "band" iff i - j < t (tilestore.band_member, tilestore.py:92-96).
+ *   dp_pool: band tiles, FP64, column-major tile order (column j, then row i).
+ *   sp_pool: off-band tiles, FP32 (MP only), same order.
+ *   scratch: FP32 panel scratch (MP only), mt_scratch_tiles(p, t) tiles:
+ *            narrowed L_kk and narrowed band-panel mirrors (factor.py:255,262).
+ *   status:  int64[4] device: [0] first failing global pivot (-1 = none),
+ *            [1] FP32 narrowing overflow count, [2] duplicate-location pairs.
+ */
+typedef struct mt_tiles {
+  int64_t n;
+  int32_t nb;
+  int32_t p;     /* ceil(n / nb) */
+  int32_t t;     /* resolved band thickness; p in DP mode */
+  int32_t mode;  /* MT_MODE_* */
+  double* dp_pool;
+  float* sp_pool;
+  float* scratch;
+  int64_t* status;
+} mt_tiles;
+
+/* Matern parameters + per-theta Bessel constants (covmath.py:72-95, 228-283),
+ * filled on the host by mt_matern_prepare(). */
+typedef struct mt_matern {
+  double variance, spatial_range, smoothness;
+  int32_t kind;      /* 0: nu = 0.5 closed form, 1: nu = 1.5 closed form, 2: Bessel */
+  int32_t nl;        /* int(nu + 1/2) upward recurrences */
+  double mu;         /* nu - nl, in [-1/2, 1/2] */
+  double gam1, gam2; /* Temme gammas */
+  double rp, rm;     /* 1/Gamma(1+mu), 1/Gamma(1-mu) */
+  double fact;       /* 1/sinc(mu) */
+  double scale;      /* variance 2^(1-nu) / Gamma(nu) */
+} mt_matern;
+
+/* sizes of the pools for a layout (element counts are tiles * nb * nb) */
+int64_t mt_dp_tiles(int32_t p, int32_t t, int32_t mode);
+int64_t mt_sp_tiles(int32_t p, int32_t t, int32_t mode);
+int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode);
+int32_t mt_version(void);
+const char* mt_last_error(void);
+
+/* Covariance tile generation: FP64 band tiles, FP32 off-band tiles written
+ * directly, DST off-band tiles absent; padding set.  Overflow of a finite
+ * value on narrowing increments status[1].
+ * Replaces TileAssembler.assemble / assemble_covariance (tilestore.py:243-262).
+ * locs: device, n x 2 row-major FP64. */
+int mt_generate(const mt_tiles* g, const double* locs, int32_t metric, double radius,
+                const mt_matern* theta, void* stream);
+
+/* Duplicate-location scan: status[2] += #pairs a<b with distance == 0
+ * (TileAssembler.__init__, tilestore.py:225-241). */
+int mt_scan_duplicates(const mt_tiles* g, const double* locs, int32_t metric, double radius,
+                       void* stream);
+
+/* Matern covariance at m distances (covmath.matern_array, covmath.py:261-283). */
+int mt_matern_array(const double* r, int64_t m, const mt_matern* theta, double* out,
+                    void* stream);
+
+/* Band-precision tile Cholesky in place (factor.cholesky, factor.py:230-285):
+ * POTRF/TRSM/SYRK/GEMM right-looking with `lookahead` (0 or 1) on a private
+ * high-priority panel stream joined back to `stream`.  A non-positive pivot
+ * sets status[0] to the global 0-based index (FactorizationError.index). */
+int mt_cholesky(const mt_tiles* g, int32_t lookahead, void* stream);
+
+/* Device scratch (doubles) needed by mt_logdet / mt_quad / mt_evaluate:
+ * p*nb + 2048 + p. */
+int64_t mt_work_doubles(const mt_tiles* g);
+
+/* log det = 2 sum log diag(L) (factor.logdet, factor.py:318-323) -> *out (device);
+ * work: >= p device doubles. */
+int mt_logdet(const mt_tiles* g, double* work, double* out, void* stream);
+
+/* In-place solves on device rhs x (n_pad x nrhs row-major, n_pad = p*nb,
+ * rows >= n must be zero): which = 1 forward L y = b, 2 backward L^T x = y,
+ * 3 both (factor.solve, factor.py:292-315). */
+int mt_solve(const mt_tiles* g, double* x, int64_t nrhs, int32_t which, void* stream);
+
+/* quad = z^T (L L^T)^{-1} z = ||L^{-1} z||^2 by the forward sweep only;
+ * z: device n_pad doubles (zero padded); work: mt_work_doubles() device
+ * doubles; *out (device). (mle._evaluate, mle.py:80-86) */
+int mt_quad(const mt_tiles* g, const double* z, double* work, double* out, void* stream);
+
+/* out = L v (factor.matvec_lower, factor.py:326-340); v, out device n_pad. */
+int mt_matvec_lower(const mt_tiles* g, const double* v, double* out, void* stream);
+
+/* One fused likelihood evaluation: generate -> cholesky -> logdet -> quad.
+ * out2 (device): [logdet, quad]; work: mt_work_doubles() device doubles.
+ * The caller resets status before and reads it after (mt_read_status).
+ * (mle._evaluate, mle.py:80-86) */
+int mt_evaluate(const mt_tiles* g, const double* locs, int32_t metric, double radius,
+                const mt_matern* theta, const double* z, double* work, double* out2,
+                int32_t lookahead, void* stream);
+
+/* Synchronise `stream` and read status: *bad_pivot (-1 none), *overflow,
+ * *duplicates.  Returns MT_E_NOT_SPD / MT_E_OVERFLOW when set, else MT_OK. */
+int mt_read_status(const mt_tiles* g, int64_t* bad_pivot, int64_t* overflow,
+                   int64_t* duplicates, void* stream);
+
+/* Reset status to {-1, 0, 0, 0} (async). */
+int mt_reset_status(const mt_tiles* g, void* stream);
+
+/* Tile transfer for the host view and TileMatrix.from_dense (tilestore.py:167-205):
+ * which = 0 FP64 payload (band pool), 1 FP32 payload (off-band pool).
+ * Host buffers are rows x cols COLUMN-major (numpy Fortran order, the
+ * reference's tile layout); rows/cols = logical (unpadded) tile shape. */
+int mt_get_tile(const mt_tiles* g, int32_t i, int32_t j, int32_t which, void* host, void* stream);
+int mt_put_tile(const mt_tiles* g, int32_t i, int32_t j, int32_t which, const void* host,
+                void* stream);
+
+/* Host-buffer end-to-end evaluation (the FFI-facing call): allocates device
+ * memory, copies locs (n x 2) and z (n) in, runs mt_evaluate, copies
+ * [logdet, quad] out, frees.  Returns MT_E_NOT_SPD with *bad_pivot set on an
+ * indefinite covariance. (mle.loglik, mle.py:89-99 minus the final affine) */
+int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t, const double* locs,
+                     const double* z, int32_t metric, double radius, const mt_matern* theta,
+                     double* out2, int64_t* bad_pivot);
+
+/* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */
+int mt_matern_prepare(double variance, double spatial_range, double smoothness,
+                      mt_matern* theta);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIXTILE_B200_H */

@@ -1,0 +1,408 @@
+// C ABI + host-side scheduler of the tile Cholesky (replaces the reference's
+// Python task graph and thread pool, factor.py:44-80,152-206,230-285).
+//
+// The right-looking DAG is issued as a stream/event schedule with lookahead 1:
+//   panel stream (high priority):  upd(k -> column k+1), POTRF(k+1), TRSM(k+1)
+//   caller stream:                 upd(k -> columns k+2 .. p-1)
+// joined by two events per step, so the panel of step k+1 runs underneath the
+// bulk update of step k.  Every tile still receives its updates in ascending
+// k from exactly one kernel per step, so results equal the lookahead-0 order
+// bit for bit (the reference's schedule invariance, factor.py:13-16).
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <vector>
+
+#include "mt_grid.cuh"
+
+// kernels (other translation units)
+int mt_generate_impl(const Grid& g, const double* locs, int metric, double radius,
+                     const mt_matern& th, cudaStream_t st);
+int mt_scan_duplicates_impl(const Grid& g, const double* locs, int metric, double radius,
+                            cudaStream_t st);
+int mt_matern_array_impl(const double* r, int64_t m, const mt_matern& th, double* out,
+                         cudaStream_t st);
+int mt_potrf_impl(const Grid& g, int k, int narrow, cudaStream_t st);
+int mt_trsm_impl(const Grid& g, int k, cudaStream_t st);
+int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st);
+int mt_logdet_impl(const Grid& g, double* out, double* work, cudaStream_t st);
+int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_t st);
+int mt_quad_impl(const Grid& g, const double* z, double* work, double* out, cudaStream_t st);
+int mt_matvec_lower_impl(const Grid& g, const double* v, double* out, cudaStream_t st);
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[512] = "";
+
+void mt_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int mt_cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  mt_set_error("%s: %s", what, cudaGetErrorString(e));
+  return 1;
+}
+
+#define CK(call, what) \
+  do { if (mt_cuda_check((call), what)) return MT_E_CUDA; } while (0)
+#define RC(call) \
+  do { int rc__ = (call); if (rc__) return rc__; } while (0)
+
+static int check_layout(const mt_tiles* g) {
+  if (!g || g->n < 1 || g->nb < 1 || g->p != (int32_t)((g->n + g->nb - 1) / g->nb) ||
+      g->t < 1 || g->t > g->p || g->mode < 0 || g->mode > 2 ||
+      (g->mode == MT_MODE_DP && g->t != g->p) || !g->dp_pool || !g->status ||
+      (g->mode == MT_MODE_MP && g->t < g->p && (!g->sp_pool || !g->scratch))) {
+    mt_set_error("bad tile layout descriptor");
+    return MT_E_BAD_ARG;
+  }
+  return MT_OK;
+}
+
+// ------------------------------------------------------ per-device context
+namespace {
+struct DevCtx {
+  cudaStream_t panel = nullptr;
+  std::vector<cudaEvent_t> ev;
+  size_t next = 0;
+  cudaEvent_t event() {
+    cudaEvent_t e = ev[next];
+    next = (next + 1) % ev.size();
+    return e;
+  }
+};
+std::mutex g_ctx_mu;
+DevCtx* g_ctx[64] = {nullptr};
+
+DevCtx* dev_ctx() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  if (!g_ctx[dev]) {
+    DevCtx* c = new DevCtx();
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&c->panel, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      delete c;
+      return nullptr;
+    }
+    c->ev.resize(16);
+    for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    g_ctx[dev] = c;
+  }
+  return g_ctx[dev];
+}
+}  // namespace
+
+// ------------------------------------------------------------------ the DAG
+static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main) {
+  const int p = g.p;
+  auto narrow_k = [&](int k) { return (g.mode == MT_MODE_MP && k + g.t <= p - 1) ? 1 : 0; };
+  if (!lookahead || p < 3) {
+    for (int k = 0; k < p; ++k) {
+      RC(mt_potrf_impl(g, k, narrow_k(k), main));
+      if (k + 1 < p) {
+        RC(mt_trsm_impl(g, k, main));
+        RC(mt_update_impl(g, k, k + 1, p, main));
+      }
+    }
+    return MT_OK;
+  }
+  DevCtx* ctx = dev_ctx();
+  if (!ctx) { mt_set_error("cannot create the panel stream"); return MT_E_CUDA; }
+  cudaStream_t pan = ctx->panel;
+  cudaEvent_t e = ctx->event();
+  CK(cudaEventRecord(e, main), "event record");
+  CK(cudaStreamWaitEvent(pan, e, 0), "stream wait");
+  RC(mt_potrf_impl(g, 0, narrow_k(0), pan));
+  RC(mt_trsm_impl(g, 0, pan));
+  for (int k = 0; k < p - 1; ++k) {
+    cudaEvent_t ep = ctx->event();
+    CK(cudaEventRecord(ep, pan), "event record");   // panel k ready
+    CK(cudaStreamWaitEvent(main, ep, 0), "stream wait");
+    // panel stream: column k+1 with panel k, then factor panel k+1
+    RC(mt_update_impl(g, k, k + 1, k + 2, pan));
+    RC(mt_potrf_impl(g, k + 1, narrow_k(k + 1), pan));
+    if (k + 2 < p) RC(mt_trsm_impl(g, k + 1, pan));
+    // caller stream: the rest of step k's trailing update
+    RC(mt_update_impl(g, k, k + 2, p, main));
+    cudaEvent_t em = ctx->event();
+    CK(cudaEventRecord(em, main), "event record");  // step k fully applied
+    CK(cudaStreamWaitEvent(pan, em, 0), "stream wait");
+  }
+  cudaEvent_t ef = ctx->event();
+  CK(cudaEventRecord(ef, pan), "event record");
+  CK(cudaStreamWaitEvent(main, ef, 0), "stream wait");
+  return MT_OK;
+}
+
+// ---------------------------------------------------------------- host math
+namespace {
+const double kLz[9] = {0.99999999999980993, 676.5203681218851,    -1259.1392167224028,
+                       771.32342877765313,  -176.61502916214059,  12.507343278686905,
+                       -0.13857109526572012, 9.9843695780195716e-6, 1.5056327351493116e-7};
+double lanczos_gamma(double x) {  // covmath.py:40-49
+  if (x < 0.5) return M_PI / (sin(M_PI * x) * lanczos_gamma(1.0 - x));
+  x -= 1.0;
+  double a = kLz[0];
+  for (int i = 1; i < 9; ++i) a += kLz[i] / (x + i);
+  double t = x + 7.0 + 0.5;
+  return sqrt(2.0 * M_PI) * pow(t, x + 0.5) * exp(-t) * a;
+}
+double zeta_odd(int idx) {  // covmath.py:52-66 (sum k^-s, k < 60, + Euler-Maclaurin tail)
+  const int s = 3 + 2 * idx, m = 60;
+  double tot = 0.0;
+  for (int k = 1; k < m; ++k) tot += pow((double)k, -s);
+  tot += pow((double)m, 1 - s) / (s - 1);
+  tot += 0.5 * pow((double)m, -s);
+  tot += s * pow((double)m, -s - 1) / 12.0;
+  tot -= s * (s + 1.0) * (s + 2.0) * pow((double)m, -s - 3) / 720.0;
+  tot += s * (s + 1.0) * (s + 2.0) * (s + 3.0) * (s + 4.0) * pow((double)m, -s - 5) / 30240.0;
+  return tot;
+}
+}  // namespace
+
+extern "C" {
+
+int32_t mt_version(void) { return 10; }
+const char* mt_last_error(void) { return g_err; }
+
+int64_t mt_dp_tiles(int32_t p, int32_t t, int32_t mode) {
+  if (mode == MT_MODE_DP) t = p;
+  Grid g{};
+  g.p = p; g.t = t; g.mode = mode;
+  return g.bcol(p);
+}
+int64_t mt_sp_tiles(int32_t p, int32_t t, int32_t mode) {
+  if (mode != MT_MODE_MP) return 0;
+  Grid g{};
+  g.p = p; g.t = t; g.mode = mode;
+  return g.scol(p);
+}
+int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode) {
+  return (mode == MT_MODE_MP && t < p) ? 2 * (int64_t)t : 0;
+}
+
+int mt_matern_prepare(double variance, double spatial_range, double smoothness, mt_matern* th) {
+  if (!th || !(variance > 0) || !(spatial_range > 0) || !(smoothness > 0) || !isfinite(variance) ||
+      !isfinite(spatial_range) || !isfinite(smoothness)) {
+    mt_set_error("Matern parameters must be finite and > 0");
+    return MT_E_BAD_ARG;
+  }
+  memset(th, 0, sizeof(*th));
+  th->variance = variance;
+  th->spatial_range = spatial_range;
+  th->smoothness = smoothness;
+  th->kind = smoothness == 0.5 ? 0 : (smoothness == 1.5 ? 1 : 2);
+  th->nl = (int32_t)(smoothness + 0.5);
+  const double mu = smoothness - th->nl;
+  th->mu = mu;
+  // Temme gammas (covmath.py:72-95)
+  const double gp = 1.0 / lanczos_gamma(1.0 + mu);
+  const double gm = 1.0 / lanczos_gamma(1.0 - mu);
+  th->rp = gp;
+  th->rm = gm;
+  th->gam2 = 0.5 * (gm + gp);
+  if (fabs(mu) >= 0.1) {
+    th->gam1 = (gm - gp) / (2.0 * mu);
+  } else if (mu == 0.0) {
+    th->gam1 = -0.5772156649015329;
+  } else {
+    double acc = 0.5772156649015329, mu2 = mu * mu, mp = mu2;
+    for (int idx = 0; idx < 10; ++idx) {
+      acc += zeta_odd(idx) * mp / (3 + 2 * idx);
+      mp *= mu2;
+    }
+    th->gam1 = gp * expm1(-2.0 * mu * acc) / (2.0 * mu);
+  }
+  th->fact = mu != 0.0 ? 1.0 / (sin(M_PI * mu) / (M_PI * mu)) : 1.0;  // 1/np.sinc(mu)
+  th->scale = variance * pow(2.0, 1.0 - smoothness) / lanczos_gamma(smoothness);
+  return MT_OK;
+}
+
+int mt_generate(const mt_tiles* t, const double* locs, int32_t metric, double radius,
+                const mt_matern* theta, void* stream) {
+  RC(check_layout(t));
+  if (!locs || !theta) { mt_set_error("null locations/theta"); return MT_E_BAD_ARG; }
+  return mt_generate_impl(make_grid(t), locs, metric, radius, *theta, (cudaStream_t)stream);
+}
+
+int mt_scan_duplicates(const mt_tiles* t, const double* locs, int32_t metric, double radius,
+                       void* stream) {
+  RC(check_layout(t));
+  return mt_scan_duplicates_impl(make_grid(t), locs, metric, radius, (cudaStream_t)stream);
+}
+
+int mt_matern_array(const double* r, int64_t m, const mt_matern* theta, double* out,
+                    void* stream) {
+  if (!theta || (m > 0 && (!r || !out))) { mt_set_error("null argument"); return MT_E_BAD_ARG; }
+  return mt_matern_array_impl(r, m, *theta, out, (cudaStream_t)stream);
+}
+
+int mt_cholesky(const mt_tiles* t, int32_t lookahead, void* stream) {
+  RC(check_layout(t));
+  return cholesky_schedule(make_grid(t), lookahead, (cudaStream_t)stream);
+}
+
+int64_t mt_work_doubles(const mt_tiles* t) {
+  return (int64_t)t->p * t->nb + 2048 + t->p;
+}
+
+int mt_logdet(const mt_tiles* t, double* work, double* out, void* stream) {
+  RC(check_layout(t));
+  return mt_logdet_impl(make_grid(t), out, work, (cudaStream_t)stream);
+}
+
+int mt_solve(const mt_tiles* t, double* x, int64_t nrhs, int32_t which, void* stream) {
+  RC(check_layout(t));
+  if (nrhs < 1 || which < 1 || which > 3) { mt_set_error("bad solve arguments"); return MT_E_BAD_ARG; }
+  return mt_solve_impl(make_grid(t), x, nrhs, which, (cudaStream_t)stream);
+}
+
+int mt_quad(const mt_tiles* t, const double* z, double* work, double* out, void* stream) {
+  RC(check_layout(t));
+  return mt_quad_impl(make_grid(t), z, work, out, (cudaStream_t)stream);
+}
+
+int mt_matvec_lower(const mt_tiles* t, const double* v, double* out, void* stream) {
+  RC(check_layout(t));
+  return mt_matvec_lower_impl(make_grid(t), v, out, (cudaStream_t)stream);
+}
+
+int mt_reset_status(const mt_tiles* t, void* stream) {
+  RC(check_layout(t));
+  const int64_t init[4] = {-1, 0, 0, 0};
+  CK(cudaMemcpyAsync(t->status, init, sizeof(init), cudaMemcpyHostToDevice, (cudaStream_t)stream),
+     "status reset");
+  // the host array is on the stack: make the copy complete before returning
+  CK(cudaStreamSynchronize((cudaStream_t)stream), "status reset sync");
+  return MT_OK;
+}
+
+int mt_evaluate(const mt_tiles* t, const double* locs, int32_t metric, double radius,
+                const mt_matern* theta, const double* z, double* work, double* out2,
+                int32_t lookahead, void* stream) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  cudaStream_t st = (cudaStream_t)stream;
+  RC(mt_generate_impl(g, locs, metric, radius, *theta, st));
+  RC(cholesky_schedule(g, lookahead, st));
+  const int64_t npad = (int64_t)g.p * g.nb;
+  RC(mt_logdet_impl(g, out2, work + npad + 2048, st));
+  RC(mt_quad_impl(g, z, work, out2 + 1, st));
+  return MT_OK;
+}
+
+int mt_read_status(const mt_tiles* t, int64_t* bad_pivot, int64_t* overflow, int64_t* dups,
+                   void* stream) {
+  RC(check_layout(t));
+  int64_t h[4];
+  CK(cudaMemcpyAsync(h, t->status, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+     "status read");
+  CK(cudaStreamSynchronize((cudaStream_t)stream), "status sync");
+  if (bad_pivot) *bad_pivot = h[0];
+  if (overflow) *overflow = h[1];
+  if (dups) *dups = h[2];
+  if (h[1] > 0) { mt_set_error("%lld value(s) exceed FP32 range during narrowing", (long long)h[1]); return MT_E_OVERFLOW; }
+  if (h[0] >= 0) { mt_set_error("matrix not positive definite at global pivot %lld", (long long)h[0]); return MT_E_NOT_SPD; }
+  return MT_OK;
+}
+
+// host tile transfer: host buffer is (rows_i x rows_j) column-major
+static int tile_xfer(const mt_tiles* t, int32_t i, int32_t j, int32_t which, void* host, bool get,
+                     cudaStream_t st) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  if (i < 0 || j < 0 || i >= g.p || j > i || !g.present(i, j) || (which == 0) != g.band(i, j)) {
+    mt_set_error("tile (%d,%d) not stored in the requested pool", i, j);
+    return MT_E_BAD_ARG;
+  }
+  const int nb = g.nb, ri = g.rows(i), rj = g.rows(j);
+  const size_t es = which == 0 ? 8 : 4;
+  void* dev = which == 0 ? (void*)g.dtile(i, j) : (void*)g.stile(i, j);
+  std::vector<unsigned char> buf((size_t)nb * nb * es);
+  if (get) {
+    CK(cudaMemcpyAsync(buf.data(), dev, buf.size(), cudaMemcpyDeviceToHost, st), "tile get");
+    CK(cudaStreamSynchronize(st), "tile get sync");
+    for (int r = 0; r < ri; ++r)
+      for (int c = 0; c < rj; ++c)
+        memcpy((unsigned char*)host + ((size_t)c * ri + r) * es, &buf[((size_t)r * nb + c) * es], es);
+  } else {
+    memset(buf.data(), 0, buf.size());
+    for (int r = 0; r < nb; ++r)
+      for (int c = 0; c < nb; ++c) {
+        unsigned char* d = &buf[((size_t)r * nb + c) * es];
+        if (r < ri && c < rj) {
+          memcpy(d, (const unsigned char*)host + ((size_t)c * ri + r) * es, es);
+        } else if (i == j && r == c) {  // padded diagonal -> identity
+          if (es == 8) { double one = 1.0; memcpy(d, &one, 8); }
+          else { float one = 1.0f; memcpy(d, &one, 4); }
+        }
+      }
+    CK(cudaMemcpyAsync(dev, buf.data(), buf.size(), cudaMemcpyHostToDevice, st), "tile put");
+    CK(cudaStreamSynchronize(st), "tile put sync");
+  }
+  return MT_OK;
+}
+
+int mt_get_tile(const mt_tiles* t, int32_t i, int32_t j, int32_t which, void* host, void* stream) {
+  return tile_xfer(t, i, j, which, host, true, (cudaStream_t)stream);
+}
+int mt_put_tile(const mt_tiles* t, int32_t i, int32_t j, int32_t which, const void* host,
+                void* stream) {
+  return tile_xfer(t, i, j, which, (void*)host, false, (cudaStream_t)stream);
+}
+
+int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t_, const double* locs,
+                     const double* z, int32_t metric, double radius, const mt_matern* theta,
+                     double* out2, int64_t* bad_pivot) {
+  if (n < 1 || nb < 1 || !locs || !z || !theta || !out2) { mt_set_error("bad arguments"); return MT_E_BAD_ARG; }
+  mt_tiles t{};
+  t.n = n; t.nb = nb; t.p = (int32_t)((n + nb - 1) / nb);
+  t.mode = mode; t.t = mode == MT_MODE_DP ? t.p : t_;
+  if (t.t < 1 || t.t > t.p) { mt_set_error("diag_thick out of range"); return MT_E_BAD_ARG; }
+  const int64_t te = (int64_t)nb * nb, npad = (int64_t)t.p * nb;
+  const size_t b_dp = mt_dp_tiles(t.p, t.t, mode) * te * 8, b_sp = mt_sp_tiles(t.p, t.t, mode) * te * 4,
+               b_sc = mt_scratch_tiles(t.p, t.t, mode) * te * 4;
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  double *d_locs = nullptr, *d_z = nullptr, *d_work = nullptr, *d_out = nullptr;
+  int rc = MT_OK;
+  auto al = [&](void** p, size_t b) { return mt_cuda_check(cudaMallocAsync(p, b ? b : 16, st), "alloc"); };
+  if (al((void**)&t.dp_pool, b_dp) || al((void**)&t.sp_pool, b_sp) || al((void**)&t.scratch, b_sc) ||
+      al((void**)&t.status, 32) || al((void**)&d_locs, npad * 16) || al((void**)&d_z, npad * 8) ||
+      al((void**)&d_work, mt_work_doubles(&t) * 8) || al((void**)&d_out, 16)) {
+    rc = MT_E_CUDA;
+  }
+  if (!rc) {
+    const int64_t init[4] = {-1, 0, 0, 0};
+    cudaMemcpyAsync(t.status, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(d_z, 0, npad * 8, st);
+    cudaMemcpyAsync(d_locs, locs, n * 16, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_z, z, n * 8, cudaMemcpyHostToDevice, st);
+    rc = mt_evaluate(&t, d_locs, metric, radius, theta, d_z, d_work, d_out, 1, st);
+    if (!rc) {
+      double h[2];
+      cudaMemcpyAsync(h, d_out, 16, cudaMemcpyDeviceToHost, st);
+      int64_t bp = -1;
+      rc = mt_read_status(&t, &bp, nullptr, nullptr, st);
+      if (bad_pivot) *bad_pivot = bp;
+      out2[0] = h[0];
+      out2[1] = h[1];
+    }
+  }
+  cudaFreeAsync(t.dp_pool, st); cudaFreeAsync(t.sp_pool, st); cudaFreeAsync(t.scratch, st);
+  cudaFreeAsync(t.status, st); cudaFreeAsync(d_locs, st); cudaFreeAsync(d_z, st);
+  cudaFreeAsync(d_work, st); cudaFreeAsync(d_out, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Tile-grid layout shared by every kernel and the host scheduler.
+//
+// Lower tile grid of an n x n SPD matrix, p = ceil(n/nb) tiles per side,
+// tiles nb x nb row-major and padded (identity on the padded diagonal).
+// Band tiles (i - j < t) live in an FP64 pool, off-band tiles in an FP32
+// pool (MP) or nowhere (DST).  Both pools are ordered column by column
+// (tile column j, then tile row i), so panel k and "all trailing tiles of
+// step k" are contiguous slot ranges: the panel TRSM and the trailing update
+// of a step each launch over one range.  (Reference layout: dict of
+// Fortran-ordered tiles, tilestore.py:139-205.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mixtile_b200.h"
+
+#define MT_HD __host__ __device__ __forceinline__
+
+struct Grid {
+  int64_t n;
+  int nb, p, t, mode;
+  double* dp;
+  float* sp;
+  float* scratch;
+  int64_t* status;
+
+  MT_HD int64_t tile_elems() const { return (int64_t)nb * nb; }
+  MT_HD bool band(int i, int j) const { return (i - j) < t; }
+  MT_HD bool present(int i, int j) const { return mode != MT_MODE_DST || (i - j) < t; }
+  // logical rows of tile row i (ragged edge, tilestore.py:154-156)
+  MT_HD int rows(int i) const {
+    int64_t r = n - (int64_t)i * nb;
+    return r < nb ? (int)r : nb;
+  }
+
+  // first band-pool slot of tile column j: sum_{j'<j} min(t, p - j')
+  MT_HD int64_t bcol(int j) const {
+    int64_t q = p - t;
+    if (j <= q) return (int64_t)j * t;
+    int64_t a = p - j;
+    return q * t + ((int64_t)t * (t + 1) - a * (a + 1)) / 2;
+  }
+  // first off-band-pool slot of tile column j: sum_{j'<j} max(0, p - t - j')
+  MT_HD int64_t scol(int j) const {
+    int64_t q = p - t;
+    if (q <= 0) return 0;
+    if (j >= q) return q * (q + 1) / 2;
+    return (int64_t)j * q - (int64_t)j * (j - 1) / 2;
+  }
+  MT_HD int64_t nband() const { return bcol(p); }
+  MT_HD int64_t noff() const { return mode == MT_MODE_MP ? scol(p) : 0; }
+
+  MT_HD double* dtile(int i, int j) const { return dp + (bcol(j) + (i - j)) * tile_elems(); }
+  MT_HD float* stile(int i, int j) const { return sp + (scol(j) + (i - j - t)) * tile_elems(); }
+
+  // scratch ring: slot s holds [narrowed L_kk][mirrors of band panel rows k+1..k+t-1]
+  MT_HD float* sdiag(int k) const { return scratch + (int64_t)(k & 1) * t * tile_elems(); }
+  MT_HD float* smirror(int i, int k) const { return sdiag(k) + (int64_t)(i - k) * tile_elems(); }
+  // FP32 operand for tile (i,k) of panel k in an FP32 update: payload or mirror
+  MT_HD const float* sp_operand(int i, int k) const {
+    return band(i, k) ? smirror(i, k) : stile(i, k);
+  }
+
+  // slot -> (i, j) inversion by binary search over the column starts
+  __device__ __forceinline__ void band_slot_ij(int64_t s, int& i, int& j) const {
+    int lo = 0, hi = p;  // find largest j with bcol(j) <= s
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (bcol(mid) <= s) lo = mid; else hi = mid;
+    }
+    j = lo;
+    i = lo + (int)(s - bcol(lo));
+  }
+  __device__ __forceinline__ void off_slot_ij(int64_t s, int& i, int& j) const {
+    int lo = 0, hi = p - t;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (scol(mid) <= s) lo = mid; else hi = mid;
+    }
+    j = lo;
+    i = lo + t + (int)(s - scol(lo));
+  }
+  __device__ __forceinline__ bool failed() const {
+    return *(volatile int64_t*)status >= 0;
+  }
+};
+
+inline Grid make_grid(const mt_tiles* g) {
+  Grid r;
+  r.n = g->n; r.nb = g->nb; r.p = g->p; r.t = g->t; r.mode = g->mode;
+  r.dp = g->dp_pool; r.sp = g->sp_pool; r.scratch = g->scratch; r.status = g->status;
+  return r;
+}
+
+// status slots
+#define MT_ST_PIVOT 0
+#define MT_ST_OVERFLOW 1
+#define MT_ST_DUP 2
+
+// error plumbing shared by the translation units
+void mt_set_error(const char* fmt, ...);
+int mt_cuda_check(cudaError_t e, const char* what);
+#define MT_LAUNCH_CHECK(what) \
+  do { if (mt_cuda_check(cudaGetLastError(), what)) return MT_E_CUDA; } while (0)

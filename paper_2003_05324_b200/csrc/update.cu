@@ -1,0 +1,244 @@
+// Trailing update of step k over tile columns [jlo, jhi):
+//   C_ij <- C_ij - A_ik A_jk^T   for k < j <= i < p   (kernels.syrk / kernels.gemm,
+//                                                     factor.py:266-274)
+// Band outputs (i - j < t) run in FP64; an off-band operand (FP32 payload) is
+// widened in registers on load, which is bit-identical to the reference's
+// materialised widened copy (factor.py:265, test_factor.py:146-153).  SYRK
+// outputs (i == j) touch the lower triangle only.  Off-band outputs (MP)
+// run in FP32 against the FP32 payload / narrowed band mirror.
+//
+// Each output tile's updates are applied by exactly one CTA per sub-tile and
+// step, in ascending k -- no split-K, no atomics -- so results are
+// deterministic and schedule-invariant (factor.py:13-16).
+#include "mt_grid.cuh"
+
+namespace {
+
+// ---------------------------------------------------------------- FP32 SIMT
+// 128x128 CTA tile, BK=8, 256 threads x (8x8) outputs, register double buffering.
+constexpr int SBM = 128, SBK = 8;
+
+__global__ void __launch_bounds__(256)
+    sgemm_update_kernel(Grid g, int k, int64_t slot0, int nsub) {
+  if (g.failed()) return;
+  const int64_t slot = slot0 + blockIdx.x / (nsub * nsub);
+  const int sub = blockIdx.x % (nsub * nsub);
+  int i, j;
+  g.off_slot_ij(slot, i, j);
+  const int nb = g.nb;
+  const int m0 = (sub / nsub) * SBM, n0 = (sub % nsub) * SBM;
+  const float* __restrict__ A = g.stile(i, k) + (int64_t)m0 * nb;
+  const float* __restrict__ B = g.sp_operand(j, k) + (int64_t)n0 * nb;
+  float* __restrict__ C = g.stile(i, j);
+
+  __shared__ __align__(16) float As[2][SBK][SBM];
+  __shared__ __align__(16) float Bs[2][SBK][SBM];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int lr = tid >> 1, lc = (tid & 1) * 4;  // load: row lr, cols lc..lc+3
+
+  float acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.f;
+
+  float4 ra = *(const float4*)(A + (int64_t)lr * nb + lc);
+  float4 rb = *(const float4*)(B + (int64_t)lr * nb + lc);
+  As[0][lc + 0][lr] = ra.x; As[0][lc + 1][lr] = ra.y; As[0][lc + 2][lr] = ra.z; As[0][lc + 3][lr] = ra.w;
+  Bs[0][lc + 0][lr] = rb.x; Bs[0][lc + 1][lr] = rb.y; Bs[0][lc + 2][lr] = rb.z; Bs[0][lc + 3][lr] = rb.w;
+  __syncthreads();
+  int buf = 0;
+  for (int kk = 0; kk < nb; kk += SBK) {
+    const bool more = kk + SBK < nb;
+    if (more) {
+      ra = *(const float4*)(A + (int64_t)lr * nb + kk + SBK + lc);
+      rb = *(const float4*)(B + (int64_t)lr * nb + kk + SBK + lc);
+    }
+#pragma unroll
+    for (int q = 0; q < SBK; ++q) {
+      float4 a0 = *(const float4*)&As[buf][q][ty * 4];
+      float4 a1 = *(const float4*)&As[buf][q][64 + ty * 4];
+      float4 b0 = *(const float4*)&Bs[buf][q][tx * 4];
+      float4 b1 = *(const float4*)&Bs[buf][q][64 + tx * 4];
+      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
+    }
+    if (more) {
+      const int nbuf = buf ^ 1;
+      As[nbuf][lc + 0][lr] = ra.x; As[nbuf][lc + 1][lr] = ra.y; As[nbuf][lc + 2][lr] = ra.z; As[nbuf][lc + 3][lr] = ra.w;
+      Bs[nbuf][lc + 0][lr] = rb.x; Bs[nbuf][lc + 1][lr] = rb.y; Bs[nbuf][lc + 2][lr] = rb.z; Bs[nbuf][lc + 3][lr] = rb.w;
+      __syncthreads();
+      buf = nbuf;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int r = m0 + (a < 4 ? ty * 4 + a : 64 + ty * 4 + a - 4);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4* cp = (float4*)(C + (int64_t)r * nb + n0 + h * 64 + tx * 4);
+      float4 c = *cp;
+      c.x -= acc[a][h * 4 + 0];
+      c.y -= acc[a][h * 4 + 1];
+      c.z -= acc[a][h * 4 + 2];
+      c.w -= acc[a][h * 4 + 3];
+      *cp = c;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- FP64 SIMT
+// 64x64 CTA tile, BK=8, 256 threads x (4x4); operands FP64 or FP32 (widened).
+constexpr int DBM = 64, DBK = 8;
+
+__device__ __forceinline__ double2 ld2(const void* base, bool f32, int64_t idx) {
+  if (f32) {
+    float2 v = *(const float2*)((const float*)base + idx);
+    return make_double2((double)v.x, (double)v.y);
+  }
+  return *(const double2*)((const double*)base + idx);
+}
+
+__global__ void __launch_bounds__(256)
+    dgemm_update_kernel(Grid g, int k, int64_t slot0, int nsub) {
+  if (g.failed()) return;
+  const int64_t slot = slot0 + blockIdx.x / (nsub * nsub);
+  const int sub = blockIdx.x % (nsub * nsub);
+  int i, j;
+  g.band_slot_ij(slot, i, j);
+  if (!g.present(i, k)) return;  // DST: GEMM(k; i, j) needs tile (i, k)
+  const int bm = sub / nsub, bn = sub % nsub;
+  const bool syrk = (i == j);
+  if (syrk && bn > bm) return;  // strict upper sub-tiles of a diagonal tile
+  const int nb = g.nb;
+  const int m0 = bm * DBM, n0 = bn * DBM;
+  const bool fa = !g.band(i, k), fb = !g.band(j, k);
+  const void* A = fa ? (const void*)g.stile(i, k) : (const void*)g.dtile(i, k);
+  const void* B = fb ? (const void*)g.stile(j, k) : (const void*)g.dtile(j, k);
+  double* __restrict__ C = g.dtile(i, j);
+
+  __shared__ __align__(16) double As[2][DBK][DBM + 2];
+  __shared__ __align__(16) double Bs[2][DBK][DBM + 2];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int lr = tid >> 2, lc = (tid & 3) * 2;
+
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+
+  const int64_t arow = (int64_t)(m0 + lr) * nb, brow = (int64_t)(n0 + lr) * nb;
+  double2 ra = ld2(A, fa, arow + lc), rb = ld2(B, fb, brow + lc);
+  As[0][lc][lr] = ra.x; As[0][lc + 1][lr] = ra.y;
+  Bs[0][lc][lr] = rb.x; Bs[0][lc + 1][lr] = rb.y;
+  __syncthreads();
+  int buf = 0;
+  for (int kk = 0; kk < nb; kk += DBK) {
+    const bool more = kk + DBK < nb;
+    if (more) {
+      ra = ld2(A, fa, arow + kk + DBK + lc);
+      rb = ld2(B, fb, brow + kk + DBK + lc);
+    }
+#pragma unroll
+    for (int q = 0; q < DBK; ++q) {
+      double2 a0 = *(const double2*)&As[buf][q][ty * 4];
+      double2 a1 = *(const double2*)&As[buf][q][ty * 4 + 2];
+      double2 b0 = *(const double2*)&Bs[buf][q][tx * 4];
+      double2 b1 = *(const double2*)&Bs[buf][q][tx * 4 + 2];
+      double av[4] = {a0.x, a0.y, a1.x, a1.y};
+      double bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    if (more) {
+      const int nbuf = buf ^ 1;
+      As[nbuf][lc][lr] = ra.x; As[nbuf][lc + 1][lr] = ra.y;
+      Bs[nbuf][lc][lr] = rb.x; Bs[nbuf][lc + 1][lr] = rb.y;
+      __syncthreads();
+      buf = nbuf;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = m0 + ty * 4 + a;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = n0 + tx * 4 + b;
+      if (!syrk || c <= r) C[(int64_t)r * nb + c] -= acc[a][b];
+    }
+  }
+}
+
+// ------------------------------------------------- generic (any nb) fallback
+template <bool F64>
+__global__ void __launch_bounds__(256)
+    gemm_generic_kernel(Grid g, int k, int64_t slot0, int nblk) {
+  if (g.failed()) return;
+  const int64_t slot = slot0 + blockIdx.x / nblk;
+  const int64_t e = (int64_t)(blockIdx.x % nblk) * 256 + threadIdx.x;
+  const int nb = g.nb;
+  if (e >= (int64_t)nb * nb) return;
+  const int r = (int)(e / nb), c = (int)(e % nb);
+  int i, j;
+  if (F64) {
+    g.band_slot_ij(slot, i, j);
+    if (!g.present(i, k)) return;
+    if (i == j && c > r) return;
+    const bool fa = !g.band(i, k), fb = !g.band(j, k);
+    double acc = 0.0;
+    for (int q = 0; q < nb; ++q) {
+      double a = fa ? (double)g.stile(i, k)[(int64_t)r * nb + q] : g.dtile(i, k)[(int64_t)r * nb + q];
+      double b = fb ? (double)g.stile(j, k)[(int64_t)c * nb + q] : g.dtile(j, k)[(int64_t)c * nb + q];
+      acc = fma(a, b, acc);
+    }
+    g.dtile(i, j)[e] -= acc;
+  } else {
+    g.off_slot_ij(slot, i, j);
+    const float* A = g.stile(i, k);
+    const float* B = g.sp_operand(j, k);
+    float acc = 0.f;
+    for (int q = 0; q < nb; ++q) acc = fmaf(A[(int64_t)r * nb + q], B[(int64_t)c * nb + q], acc);
+    g.stile(i, j)[e] -= acc;
+  }
+}
+
+}  // namespace
+
+int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
+  if (jlo >= jhi) return MT_OK;
+  const int nb = g.nb;
+  // band (FP64) outputs in columns [jlo, jhi)
+  const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
+  if (bcnt > 0) {
+    if (nb % DBM == 0) {
+      const int nsub = nb / DBM;
+      dgemm_update_kernel<<<(unsigned)(bcnt * nsub * nsub), 256, 0, st>>>(g, k, b0, nsub);
+    } else {
+      const int nblk = (nb * nb + 255) / 256;
+      gemm_generic_kernel<true><<<(unsigned)(bcnt * nblk), 256, 0, st>>>(g, k, b0, nblk);
+    }
+    MT_LAUNCH_CHECK("dgemm_update");
+  }
+  if (g.mode != MT_MODE_MP) return MT_OK;
+  const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
+  if (scnt > 0) {
+    if (nb % SBM == 0) {
+      const int nsub = nb / SBM;
+      sgemm_update_kernel<<<(unsigned)(scnt * nsub * nsub), 256, 0, st>>>(g, k, s0, nsub);
+    } else {
+      const int nblk = (nb * nb + 255) / 256;
+      gemm_generic_kernel<false><<<(unsigned)(scnt * nblk), 256, 0, st>>>(g, k, s0, nblk);
+    }
+    MT_LAUNCH_CHECK("sgemm_update");
+  }
+  return MT_OK;
+}

