@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark: mixed-precision Gaussian log-likelihood evaluations on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full log-likelihood evaluation of BASELINE.json configs[1]
+(N = 65,536 locations, tile 512, MP band t = 2, Matern (1, 0.1, 0.5)):
+covariance generation -> band-precision tile Cholesky -> logdet -> quadratic
+form, all on the device.  Prints ONE JSON line (rank 0).
+
+  value      whole-job loglik evaluations/s, inputs resident in HBM, device time
+             (CUDA events, max over ranks).  Also cholesky_tflops = (N^3/3)/T_chol.
+  e2e        the same metric through the public API `loglik(dataset, ...)` from
+             host numpy buffers (pinned H2D of locations + z, D2H of the result).
+  roofline   dominant kernel's achieved TFLOP/s from CUDA events recorded around
+             every launch inside the timed region vs a measured FMA peak.
+  cpu_baseline  the reference algorithm (oracle port: same LAPACK/BLAS calls as
+             the reference) on the host cores, bounded sample, extrapolated.
+  mp_vs_dp   the build's own full-DP evaluation timed the same way.
+
+With --gpus N > 1 (torchrun, one rank per GPU) every rank evaluates its own
+likelihood replica (weak scaling; the 2D block-cyclic distributed factor is
+not in this round).  --impl reference times only the CPU reference arm.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("Mixed-precision Cholesky TFLOP/s + loglik evals/s at N=262144, 1-8 B200 vs full-DP")
+UNIT = "loglik evals/s"
+THETA = (1.0, 0.1, 0.5)
+KINDS = ["gen64", "gen32", "potrf", "trsm64", "trsm32", "upd64", "upd32", "solve", "misc"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--nb", type=int, default=512)
+    ap.add_argument("--t", type=int, default=2)
+    ap.add_argument("--dp-steps", type=int, default=1)
+    ap.add_argument("--cpu-n", type=int, default=16384, help="CPU baseline sample size")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dp", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[q] for r in self.rows for q in range(4)
+                          if len(r) > 4 + q and r[4 + q].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- CPU baseline
+def cpu_reference_sample(n, nb, t, reps=1):
+    """Time the reference algorithm (oracle port) for one MP evaluation at n on
+    all host cores; returns (seconds per eval, cholesky seconds, cores, info)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info, threadpool_limits
+
+    from oracle import mixtile_oracle as O
+    from paper_2003_05324_b200.geodata import GeoDataset, derive_seed, generate_locations, morton_sort
+
+    cores = os.cpu_count() or 1
+    locs = generate_locations(n, seed=derive_seed(0, 0))
+    ds, _ = morton_sort(GeoDataset(locs, np.random.default_rng(7).standard_normal(n)))
+    best = best_chol = float("inf")
+    with threadpool_limits(limits=cores):
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            tiles = O.assemble(ds.locations, THETA, nb, "mp", t)
+            t1 = time.perf_counter()
+            fac = O.cholesky(tiles, n, nb, "mp", t)
+            t2 = time.perf_counter()
+            O.logdet(fac, -(-n // nb))
+            float(ds.z @ O.solve(fac, n, nb, ds.z))
+            t3 = time.perf_counter()
+            best = min(best, t3 - t0)
+            best_chol = min(best_chol, t2 - t1)
+        libs = [f"{d.get('internal_api')}:{d.get('num_threads')}" for d in threadpool_info()]
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    return best, best_chol, cores, {"cpu_model": cpu, "blas_threads": libs}
+
+
+def cpu_baseline_obj(args):
+    sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t)
+    scale = (args.cpu_n / args.n) ** 3
+    return {
+        "value": (1.0 / sec) * scale,
+        "unit": UNIT,
+        "cores": cores,
+        "kind": "port",
+        "sample": (f"oracle port of the reference (same dpotrf/dtrsm/strsm/dsyrk/dgemm/sgemm "
+                   f"calls) for one MP t={args.t} nb={args.nb} evaluation at N={args.cpu_n}: "
+                   f"{sec:.2f} s ({chol:.2f} s Cholesky = "
+                   f"{args.cpu_n ** 3 / 3 / chol / 1e9:.1f} GFLOP/s); value extrapolated to "
+                   f"N={args.n} by the N^3 flop count"),
+        "cpu_cholesky_gflops": args.cpu_n ** 3 / 3 / chol / 1e9,
+        **info,
+    }
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    for _ in range(max(0, args.warmup)):
+        cpu_reference_sample(args.cpu_n, args.nb, args.t)
+    times = []
+    for _ in range(max(1, args.steps)):
+        sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t)
+        times.append(sec)
+    sec = sum(times) / len(times)
+    value = (1.0 / sec) * (args.cpu_n / args.n) ** 3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+        "config": {"workload": f"configs[1] sample: MP t={args.t} nb={args.nb} N={args.cpu_n} "
+                               f"extrapolated to N={args.n}", "n": args.n, "nb": args.nb,
+                   "band_t": args.t},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"one MP evaluation at N={args.cpu_n} per step, "
+                                   f"extrapolated by N^3", **info},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_05324_b200 as mt
+    from paper_2003_05324_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    lib = _lib.load()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n, nb, t = args.n, args.nb, args.t
+    locs = mt.generate_locations(n, seed=mt.derive_seed(rank, 0))
+    z = np.random.default_rng(mt.derive_seed(rank, 1)).standard_normal(n)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, z))
+    theta = mt.MaternParams(*THETA)
+    mp_pol = mt.PrecisionPolicy.mp(diag_thick=t)
+
+    asm = mt.TileAssembler(ds, nb)
+    ev = mt.Evaluator(asm, mp_pol)
+    for _ in range(max(3, args.warmup)):
+        ev(theta)
+
+    # ---- timed region: K evaluations, inputs resident in HBM
+    clocks = ClockSampler(local_rank)
+    st = torch.cuda.current_stream()
+    barrier()
+    torch.cuda.synchronize()
+    lib.mt_prof_begin(8192)
+    l0 = lib.mt_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with clocks:
+        e0.record(st)
+        for _ in range(args.steps):
+            ev.launch(theta)
+            results.append(ev.finish())
+        e1.record(st)
+        torch.cuda.synchronize()
+    launches = lib.mt_launch_count() - l0
+    import ctypes
+    K = len(KINDS)
+    arr = [(ctypes.c_double * K)() for _ in range(3)]
+    cnt = (ctypes.c_int64 * K)()
+    lib.mt_prof_end(K, arr[0], arr[1], arr[2], cnt)
+    barrier()
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    value = args.steps * world / t_dev
+    kinds = {KINDS[q]: {"ms": arr[0][q] / args.steps, "flops": arr[1][q] / args.steps,
+                        "bytes": arr[2][q] / args.steps, "launches": cnt[q] // max(1, args.steps)}
+             for q in range(K)}
+    chol_ms = sum(kinds[k]["ms"] for k in ("potrf", "trsm64", "trsm32", "upd64", "upd32"))
+
+    # Cholesky-only device time (one extra pass, events around mt_cholesky)
+    m = ev.matrix
+    th = _lib.matern_struct(*THETA)
+    sh = _lib.stream_handle()
+    m.reset_status()
+    lib.mt_generate(ctypes.byref(m.desc), _lib.ptr(asm.d_locs), 0, 0.0, ctypes.byref(th), sh)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(st)
+    lib.mt_cholesky(ctypes.byref(m.desc), 1, sh)
+    c1.record(st)
+    torch.cuda.synchronize()
+    t_chol = max_over_ranks(c0.elapsed_time(c1) / 1e3)
+    chol_tflops = world * (n ** 3 / 3.0) / t_chol / 1e12
+
+    # ---- full-DP leg (the build's own full-DP path)
+    dp = None
+    if not args.no_dp:
+        del ev
+        torch.cuda.empty_cache()
+        evd = mt.Evaluator(asm, mt.PrecisionPolicy.dp())
+        evd(theta)
+        barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        d0.record(st)
+        for _ in range(args.dp_steps):
+            evd(theta)
+        d1.record(st)
+        torch.cuda.synchronize()
+        t_dp = max_over_ranks(d0.elapsed_time(d1) / 1e3) / args.dp_steps
+        dp = {"evals_per_s": world / t_dp, "ms_per_eval": t_dp * 1e3,
+              "mp_speedup": (world / t_dp and (value / (world / t_dp)))}
+        del evd
+        torch.cuda.empty_cache()
+
+    # ---- e2e through the public API from host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin_locs = torch.from_numpy(np.ascontiguousarray(ds.locations)).pin_memory()
+        pin_z = torch.from_numpy(np.ascontiguousarray(ds.z)).pin_memory()
+        host_ds = mt.GeoDataset(pin_locs.numpy(), pin_z.numpy())
+        mt.loglik(host_ds, theta, nb, mp_pol)  # warm the allocator
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k_e2e = max(1, min(args.steps, 3))
+        s0.record(st)
+        for _ in range(k_e2e):
+            out = mt.loglik(host_ds, theta, nb, mp_pol)
+        s1.record(st)
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(s0.elapsed_time(s1) / 1e3)
+        e2e = {"value": k_e2e * world / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(ds.locations.nbytes + ds.z.nbytes),
+               "d2h_bytes_per_step": 16 + 32 + 32,
+               "api": "paper_2003_05324_b200.loglik(dataset, params, nb, policy)",
+               "loglik": out.value}
+
+    # ---- roofline of the dominant kernel
+    dom = max(("upd32", "upd64", "potrf", "trsm64", "trsm32", "gen32", "gen64"),
+              key=lambda k: kinds[k]["ms"])
+    probe_kind = 1 if dom in ("upd64", "potrf", "trsm64") else 0
+    pk = ctypes.c_double()
+    lib.mt_peak_probe(probe_kind, 20000, ctypes.byref(pk))
+    d = kinds[dom]
+    achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
+                "frac": achieved / pk.value if pk.value else None, "traffic": traffic,
+                "kernel": dom, "pipe": "FP32 FFMA (SIMT)" if probe_kind == 0 else "FP64 DFMA",
+                "peak_source": ("measured this run by mt_peak_probe "
+                                f"({'FFMA' if probe_kind == 0 else 'DFMA'} chains on all SMs); "
+                                "MEASURED_PEAKS.json has no FP32/FP64 figure"),
+                "launches_per_step": d["launches"],
+                "avg_launch_ms": d["ms"] / max(1, d["launches"])}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_obj(args)
+
+    if rank == 0:
+        fl = mt.planned_flops(n, nb, mp_pol)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": f"BASELINE configs[1]: N={n}, tile {nb}, MP band t={t}, "
+                                   f"Matern{THETA}, one loglik eval per step",
+                       "n": n, "nb": nb, "band_t": t, "theta": list(THETA),
+                       "sp_flop_fraction": fl.sp_fraction,
+                       "l2": "inputs (tile pools) >> 126 MB L2; no flush needed",
+                       "z": "N(0,1) timing-only observations (parity runs use field z)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "cholesky_tflops": chol_tflops, "cholesky_ms": t_chol * 1e3,
+            "kernels_ms_per_step": {k: round(v["ms"], 3) for k, v in kinds.items()},
+            "mp_vs_dp": dp, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+            "loglik_sample": results[-1],
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

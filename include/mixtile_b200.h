@@ -160,6 +160,20 @@ int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t, const doubl
                      const double* z, int32_t metric, double radius, const mt_matern* theta,
                      double* out2, int64_t* bad_pivot);
 
+/* --- tracing (the reference records wall time only, cli.py:253-258) ---
+ * mt_launch_count: kernels launched by this library since load.
+ * mt_prof_begin/end: bracket every launch group with CUDA events on its own
+ * stream; end() synchronises the device and returns, per kernel kind
+ * (0 gen64, 1 gen32, 2 potrf, 3 trsm64, 4 trsm32, 5 upd64, 6 upd32, 7 solve,
+ * 8 misc), total device ms, algorithmic flops, algorithmic bytes, launches. */
+long long mt_launch_count(void);
+int mt_prof_begin(int32_t capacity);
+int mt_prof_end(int32_t nkinds, double* ms, double* flops, double* bytes, int64_t* count);
+
+/* Peak probes for roofline denominators: kind 0 FFMA, 1 DFMA, 2 FP64 DMMA;
+ * *tflops = achieved TFLOP/s of a dependent-chain FMA kernel on all SMs. */
+int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
+
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */
 int mt_matern_prepare(double variance, double spatial_range, double smoothness,
                       mt_matern* theta);

@@ -77,6 +77,10 @@ SIGNATURES = {
     "mt_reset_status": (ctypes.c_int, [_P(MtTiles), _V]),
     "mt_get_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
     "mt_put_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
+    "mt_launch_count": (ctypes.c_longlong, []),
+    "mt_prof_begin": (ctypes.c_int, [_I32]),
+    "mt_prof_end": (ctypes.c_int, [_I32, _V, _V, _V, _V]),
+    "mt_peak_probe": (ctypes.c_int, [_I32, _I32, _P(_D)]),
     "mt_evaluate_host": (ctypes.c_int, [_I64, _I32, _I32, _I32, _V, _V, _I32, _D, _P(MtMatern),
                                         _V, _P(_I64)]),
 }

@@ -218,8 +218,10 @@ int mt_generate_impl(const Grid& g, const double* locs, int metric, double radiu
   const int64_t nband = g.nband();
   // grid.x limit 2^31-1: chunk the slot range
   const int64_t max_slots = (int64_t)((1u << 31) - 1) / nrb;
+  const double te = (double)g.nb * g.nb;
   for (int64_t s0 = 0; s0 < nband; s0 += max_slots) {
     int64_t cnt = nband - s0 < max_slots ? nband - s0 : max_slots;
+    ProfScope ps(MT_K_GEN64, st, 0.0, cnt * te * 8.0);
     gen_kernel<double><<<(unsigned)(cnt * nrb), 256, 0, st>>>(g, (const double2*)locs, metric,
                                                               radius, th, s0, nrb);
     MT_LAUNCH_CHECK("gen_kernel<double>");
@@ -227,6 +229,7 @@ int mt_generate_impl(const Grid& g, const double* locs, int metric, double radiu
   const int64_t noff = g.noff();
   for (int64_t s0 = 0; s0 < noff; s0 += max_slots) {
     int64_t cnt = noff - s0 < max_slots ? noff - s0 : max_slots;
+    ProfScope ps(MT_K_GEN32, st, 0.0, cnt * te * 4.0);
     gen_kernel<float><<<(unsigned)(cnt * nrb), 256, 0, st>>>(g, (const double2*)locs, metric,
                                                              radius, th, s0, nrb);
     MT_LAUNCH_CHECK("gen_kernel<float>");
@@ -238,6 +241,7 @@ int mt_scan_duplicates_impl(const Grid& g, const double* locs, int metric, doubl
                             cudaStream_t st) {
   int64_t blocks = g.n < 148 * 16 ? g.n : 148 * 16;
   if (blocks < 1) return MT_OK;
+  ProfScope ps(MT_K_MISC, st, 0.0, 0.0);
   dup_kernel<<<(unsigned)blocks, 256, 0, st>>>((const double2*)locs, g.n, metric, radius,
                                                 g.status);
   MT_LAUNCH_CHECK("dup_kernel");
@@ -249,6 +253,7 @@ int mt_matern_array_impl(const double* r, int64_t m, const mt_matern& th, double
   if (m <= 0) return MT_OK;
   int64_t blocks = (m + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
+  ProfScope ps(MT_K_MISC, st, 0.0, m * 16.0);
   matern_array_kernel<<<(unsigned)blocks, 256, 0, st>>>(r, m, th, out);
   MT_LAUNCH_CHECK("matern_array_kernel");
   return MT_OK;

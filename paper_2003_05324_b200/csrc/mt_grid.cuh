@@ -102,3 +102,22 @@ void mt_set_error(const char* fmt, ...);
 int mt_cuda_check(cudaError_t e, const char* what);
 #define MT_LAUNCH_CHECK(what) \
   do { if (mt_cuda_check(cudaGetLastError(), what)) return MT_E_CUDA; } while (0)
+
+// launch accounting + event profiling (prof.cu)
+void mt_count_launch(int n);
+int mt_prof_start(int kind, cudaStream_t st, double flops, double bytes);
+void mt_prof_stop(int token, cudaStream_t st);
+enum MtKind {
+  MT_K_GEN64 = 0, MT_K_GEN32, MT_K_POTRF, MT_K_TRSM64, MT_K_TRSM32, MT_K_UPD64, MT_K_UPD32,
+  MT_K_SOLVE, MT_K_MISC, MT_NKINDS
+};
+// brackets the launches of one kernel group with profiling events
+struct ProfScope {
+  int tok;
+  cudaStream_t st;
+  ProfScope(int kind, cudaStream_t s, double flops, double bytes, int launches = 1) : st(s) {
+    mt_count_launch(launches);
+    tok = mt_prof_start(kind, s, flops, bytes);
+  }
+  ~ProfScope() { mt_prof_stop(tok, st); }
+};

@@ -144,6 +144,8 @@ int launch_potrf(const Grid& g, int k, int narrow, cudaStream_t st) {
   size_t smem = (size_t)(g.nb > BW ? g.nb - BW : 1) * (BW + 1) * sizeof(double);
   cudaFuncSetAttribute(potrf_kernel<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        200 * 1024);
+  const double r = g.rows(k);
+  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0, (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)));
   potrf_kernel<BW><<<1, kThreads, smem, st>>>(g, k, narrow);
   MT_LAUNCH_CHECK("potrf_kernel");
   return MT_OK;

@@ -1,0 +1,160 @@
+// Launch accounting and event profiling (the tracing subsystem; the
+// reference only records wall time, cli.py:253-258).
+//
+// Every kernel launch in the library increments a counter (mt_launch_count).
+// Between mt_prof_begin/mt_prof_end each launch group is bracketed by CUDA
+// events recorded on the stream it is launched on, tagged with a kernel kind
+// and its ALGORITHMIC flops and bytes, so bench.py can report per-kernel
+// achieved TFLOP/s or GB/s over the timed region itself.
+//
+// Also: FMA peak probes (FFMA, DFMA, FP64 DMMA) used as roofline
+// denominators where MEASURED_PEAKS.json has none.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "mt_grid.cuh"
+
+namespace {
+struct Rec {
+  int kind;
+  int ev;
+  double flops, bytes;
+};
+std::mutex g_mu;
+std::atomic<long long> g_launches{0};
+bool g_on = false;
+std::vector<cudaEvent_t> g_events;
+std::vector<Rec> g_recs;
+int g_next_ev = 0;
+}  // namespace
+
+void mt_count_launch(int n) { g_launches += n; }
+
+int mt_prof_start(int kind, cudaStream_t st, double flops, double bytes) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (!g_on || g_next_ev + 2 > (int)g_events.size()) return -1;
+  int e = g_next_ev;
+  g_next_ev += 2;
+  cudaEventRecord(g_events[e], st);
+  g_recs.push_back({kind, e, flops, bytes});
+  return e;
+}
+
+void mt_prof_stop(int token, cudaStream_t st) {
+  if (token < 0) return;
+  cudaEventRecord(g_events[token + 1], st);
+}
+
+// ------------------------------------------------------------ peak probes
+namespace {
+template <typename T>
+__global__ void __launch_bounds__(256) fma_probe(T* out, int iters, T seed) {
+  T a[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = seed + (T)(threadIdx.x + q);
+  const T b = (T)0.999999, c = (T)1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = a[q] * b + c;
+  }
+  T s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += a[q];
+  if (s == (T)-1.2345) out[0] = s;  // keep the chain alive
+}
+
+// FP64 DMMA m8n8k4 throughput probe (SASS: DMMA)
+__global__ void __launch_bounds__(256) dmma_probe(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 0.999;
+  double c[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) c[q][0] = c[q][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) s += c[q][0] + c[q][1];
+  if (s == -1.2345) out[0] = s;
+}
+}  // namespace
+
+extern "C" {
+
+long long mt_launch_count(void) { return g_launches.load(); }
+
+int mt_prof_begin(int32_t capacity) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const int need = 2 * (capacity > 0 ? capacity : 1);
+  while ((int)g_events.size() < need) {
+    cudaEvent_t e;
+    if (mt_cuda_check(cudaEventCreate(&e), "prof event")) return MT_E_CUDA;
+    g_events.push_back(e);
+  }
+  g_recs.clear();
+  g_next_ev = 0;
+  g_on = true;
+  return MT_OK;
+}
+
+// per-kind totals over the profiled region: ms[k], flops[k], bytes[k], count[k]
+int mt_prof_end(int32_t nkinds, double* ms, double* flops, double* bytes, int64_t* count) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_on = false;
+  for (int k = 0; k < nkinds; ++k) { ms[k] = flops[k] = bytes[k] = 0.0; count[k] = 0; }
+  if (mt_cuda_check(cudaDeviceSynchronize(), "prof sync")) return MT_E_CUDA;
+  for (const Rec& r : g_recs) {
+    if (r.kind < 0 || r.kind >= nkinds) continue;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, g_events[r.ev], g_events[r.ev + 1]) != cudaSuccess) continue;
+    ms[r.kind] += t;
+    flops[r.kind] += r.flops;
+    bytes[r.kind] += r.bytes;
+    count[r.kind] += 1;
+  }
+  g_recs.clear();
+  return MT_OK;
+}
+
+// kind 0: FFMA, 1: DFMA, 2: FP64 DMMA.  Returns achieved TFLOP/s in *tflops.
+int mt_peak_probe(int32_t kind, int32_t iters, double* tflops) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 8, threads = 256;
+  void* buf = nullptr;
+  if (mt_cuda_check(cudaMalloc(&buf, 64), "probe alloc")) return MT_E_CUDA;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double flop = 0.0;
+  for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+    cudaEventRecord(a);
+    if (kind == 0) {
+      fma_probe<float><<<blocks, threads>>>((float*)buf, iters, 1.0f);
+      flop = 2.0 * 8 * (double)iters * blocks * threads;
+    } else if (kind == 1) {
+      fma_probe<double><<<blocks, threads>>>((double*)buf, iters, 1.0);
+      flop = 2.0 * 8 * (double)iters * blocks * threads;
+    } else {
+      dmma_probe<<<blocks, threads>>>((double*)buf, iters);
+      flop = 2.0 * 8 * 8 * 4 * 4 * (double)iters * blocks * (threads / 32);
+    }
+    cudaEventRecord(b);
+  }
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  if (mt_cuda_check(cudaGetLastError(), "peak probe")) return MT_E_CUDA;
+  *tflops = flop / (ms * 1e-3) / 1e12;
+  return MT_OK;
+}
+
+}  // extern "C"

@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(256) matvec_lower_kernel(Grid g, const double*
 }  // namespace
 
 int mt_logdet_impl(const Grid& g, double* out, double* work, cudaStream_t st) {
+  ProfScope ps(MT_K_MISC, st, 0.0, (double)g.p * g.nb * 8.0, 2);
   logdet_partial_kernel<<<g.p, 256, 0, st>>>(g, work);
   MT_LAUNCH_CHECK("logdet_partial");
   fixed_sum_kernel<<<1, 1, 0, st>>>(work, g.p, 2.0, out);
@@ -260,7 +261,11 @@ int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_
                        (int)(smem > 48 * 1024 ? smem : 48 * 1024));
   cudaFuncSetAttribute(trsv_bwd_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(smem > 48 * 1024 ? smem : 48 * 1024));
+  // bytes: the factor is read once per sweep
+  const double fbytes = (double)g.nband() * nb * nb * 8.0 + (double)g.noff() * nb * nb * 4.0;
+  const double fflops = 2.0 * (double)g.n * g.n;  // ~n^2 multiply-adds per sweep per rhs
   if (which & 1) {
+    ProfScope ps(MT_K_SOLVE, st, fflops * nrhs, fbytes, 2 * p - 1);
     const int nrb = (nb + kGemvRows - 1) / kGemvRows;
     for (int i = 0; i < p; ++i) {
       trsv_fwd_diag_kernel<<<1, 512, smem, st>>>(g, i, x, nrhs);
@@ -272,6 +277,7 @@ int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_
     }
   }
   if (which & 2) {
+    ProfScope ps(MT_K_SOLVE, st, fflops * nrhs, fbytes, 2 * p - 1);
     const int ncb = (nb + 31) / 32;
     for (int i = p - 1; i >= 0; --i) {
       trsv_bwd_diag_kernel<<<1, 512, smem, st>>>(g, i, x, nrhs);
@@ -295,6 +301,7 @@ int mt_quad_impl(const Grid& g, const double* z, double* work, double* out, cuda
   if (rc) return rc;
   double* partial = work + npad;
   const int blocks = 1024;
+  ProfScope ps(MT_K_MISC, st, 2.0 * npad, npad * 8.0, 2);
   sumsq_partial_kernel<<<blocks, 256, 0, st>>>(work, npad, partial);
   MT_LAUNCH_CHECK("sumsq_partial");
   fixed_sum_kernel<<<1, 1, 0, st>>>(partial, blocks, 1.0, out);
@@ -304,6 +311,7 @@ int mt_quad_impl(const Grid& g, const double* z, double* work, double* out, cuda
 
 int mt_matvec_lower_impl(const Grid& g, const double* v, double* out, cudaStream_t st) {
   const int nrb = (g.nb + kGemvRows - 1) / kGemvRows;
+  ProfScope ps(MT_K_SOLVE, st, (double)g.n * g.n, (double)g.nband() * g.nb * g.nb * 8.0);
   matvec_lower_kernel<<<(unsigned)(g.p * nrb), 256, 0, st>>>(g, v, out, nrb);
   MT_LAUNCH_CHECK("matvec_lower");
   return MT_OK;

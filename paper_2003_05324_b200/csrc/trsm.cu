@@ -113,6 +113,12 @@ int launch_trsm(const Grid& g, int k, int64_t s0, int64_t cnt, int mirror_ok, cu
   size_t smem = ((size_t)kRB * (g.nb + 1) + 32 * 33) * sizeof(T);
   cudaFuncSetAttribute(trsm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  const double rk = g.rows(k), nb = g.nb;
+  // algorithmic work: rows(i) * rows(k)^2 per tile (factor.py:88-90); last row may be ragged
+  const bool last = (sizeof(T) == 8 ? (k + g.t >= g.p) : true) && cnt > 0;
+  const double rows_sum = (cnt - (last ? 1 : 0)) * nb + (last ? g.rows(g.p - 1) : 0);
+  ProfScope ps(sizeof(T) == 8 ? MT_K_TRSM64 : MT_K_TRSM32, st, rows_sum * rk * rk,
+               cnt * nb * nb * sizeof(T) * 2.0);
   trsm_kernel<T><<<(unsigned)(cnt * nrb), kThreads, smem, st>>>(g, k, s0, nrb, mirror_ok);
   MT_LAUNCH_CHECK("trsm_kernel");
   return MT_OK;

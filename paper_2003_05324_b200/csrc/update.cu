@@ -213,12 +213,34 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
+// algorithmic flops of step k's updates into columns [jlo, jhi) (factor.py:91-95)
+static void update_flops(const Grid& g, int k, int jlo, int jhi, double& f64, double& f32) {
+  f64 = f32 = 0.0;
+  const double rk = g.rows(k);
+  for (int j = jlo; j < jhi; ++j) {
+    const double rj = g.rows(j);
+    const int iband = j + g.t < g.p ? j + g.t : g.p;  // band rows [j, iband)
+    for (int i = j; i < iband; ++i) {
+      if (!g.present(i, k)) continue;
+      const double ri = g.rows(i);
+      f64 += (i == j) ? ri * ri * rk : 2.0 * ri * rj * rk;
+    }
+    if (g.mode == MT_MODE_MP && iband < g.p) {  // off-band rows [iband, p): last may be ragged
+      const double cnt = g.p - iband;
+      f32 += 2.0 * rj * rk * ((cnt - 1) * g.nb + g.rows(g.p - 1));
+    }
+  }
+}
+
 int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   if (jlo >= jhi) return MT_OK;
   const int nb = g.nb;
+  double f64, f32;
+  update_flops(g, k, jlo, jhi, f64, f32);
   // band (FP64) outputs in columns [jlo, jhi)
   const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
   if (bcnt > 0) {
+    ProfScope ps(MT_K_UPD64, st, f64, bcnt * (double)nb * nb * 8.0 * 3.0);
     if (nb % DBM == 0) {
       const int nsub = nb / DBM;
       dgemm_update_kernel<<<(unsigned)(bcnt * nsub * nsub), 256, 0, st>>>(g, k, b0, nsub);
@@ -231,6 +253,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   if (g.mode != MT_MODE_MP) return MT_OK;
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
   if (scnt > 0) {
+    ProfScope ps(MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
     if (nb % SBM == 0) {
       const int nsub = nb / SBM;
       sgemm_update_kernel<<<(unsigned)(scnt * nsub * nsub), 256, 0, st>>>(g, k, s0, nsub);

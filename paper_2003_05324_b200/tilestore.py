@@ -295,12 +295,14 @@ class TileAssembler:
         self.p = -(-self.n // self.nb)
         dev = torch.device("cuda", torch.cuda.current_device())
         npad = self.p * self.nb
-        locs = np.zeros((npad, 2))
-        locs[: self.n] = dataset.locations
-        self.d_locs = torch.from_numpy(locs).to(dev)
-        z = np.zeros(npad)
-        z[: self.n] = dataset.z
-        self.d_z = torch.from_numpy(z).to(dev)
+        # pinned staging (torch's caching host allocator) -> async H2D
+        stage = torch.zeros((npad, 3), dtype=torch.float64, pin_memory=True)
+        sv = stage.numpy()
+        sv[: self.n, :2] = dataset.locations
+        sv[: self.n, 2] = dataset.z
+        d = stage.to(dev, non_blocking=True)
+        self.d_locs = d[:, :2].contiguous()
+        self.d_z = d[:, 2].contiguous()
         self.metric_code = dataset.metric.code
         self.radius = float(dataset.metric.radius)
         probe = _Probe(self.n, self.nb, dev)
