@@ -51,6 +51,8 @@ extern "C" {
  *            narrowed L_kk and narrowed band-panel mirrors (factor.py:255,262).
  *   status:  int64[4] device: [0] first failing global pivot (-1 = none),
  *            [1] FP32 narrowing overflow count, [2] duplicate-location pairs.
+ *   split:   TF32 hi/lo split of panels k (ring of 2): tile (i, k) of panel k at
+ *            split + ((k&1)*p + i)*2*nb*nb (hi) and + nb*nb (lo).
  */
 typedef struct mt_tiles {
   int64_t n;
@@ -62,6 +64,9 @@ typedef struct mt_tiles {
   float* sp_pool;
   float* scratch;
   int64_t* status;
+  float* split;  /* optional (MP, tensor-core engine): mt_split_tiles() FP32 tiles holding
+                    the TF32 hi/lo split of the two panels in flight; NULL disables the
+                    tcgen05 3xTF32 update (FFMA fallback kernel is used instead) */
 } mt_tiles;
 
 /* Matern parameters + per-theta Bessel constants (covmath.py:72-95, 228-283),
@@ -81,6 +86,7 @@ typedef struct mt_matern {
 int64_t mt_dp_tiles(int32_t p, int32_t t, int32_t mode);
 int64_t mt_sp_tiles(int32_t p, int32_t t, int32_t mode);
 int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode);
+int64_t mt_split_tiles(int32_t p, int32_t t, int32_t mode);
 int32_t mt_version(void);
 const char* mt_last_error(void);
 
@@ -173,6 +179,11 @@ int mt_prof_end(int32_t nkinds, double* ms, double* flops, double* bytes, int64_
 /* Peak probes for roofline denominators: kind 0 FFMA, 1 DFMA, 2 FP64 DMMA;
  * *tflops = achieved TFLOP/s of a dependent-chain FMA kernel on all SMs. */
 int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
+
+/* Runtime options; returns the previous value.
+ *   0: FP32 (off-band) update engine: 0 = SIMT FFMA, 1 = tcgen05 3xTF32 (default)
+ *   1: CTA cap of the bulk trailing update (0 = all SMs) */
+int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */
 int mt_matern_prepare(double variance, double spatial_range, double smoothness,

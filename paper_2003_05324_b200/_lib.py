@@ -29,6 +29,7 @@ class MtTiles(ctypes.Structure):
         ("sp_pool", ctypes.c_void_p),
         ("scratch", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
+        ("split", ctypes.c_void_p),
     ]
 
 
@@ -62,6 +63,7 @@ SIGNATURES = {
     "mt_dp_tiles": (_I64, [_I32, _I32, _I32]),
     "mt_sp_tiles": (_I64, [_I32, _I32, _I32]),
     "mt_scratch_tiles": (_I64, [_I32, _I32, _I32]),
+    "mt_split_tiles": (_I64, [_I32, _I32, _I32]),
     "mt_work_doubles": (_I64, [_P(MtTiles)]),
     "mt_matern_prepare": (ctypes.c_int, [_D, _D, _D, _P(MtMatern)]),
     "mt_generate": (ctypes.c_int, [_P(MtTiles), _V, _I32, _D, _P(MtMatern), _V]),
@@ -77,6 +79,7 @@ SIGNATURES = {
     "mt_reset_status": (ctypes.c_int, [_P(MtTiles), _V]),
     "mt_get_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
     "mt_put_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
+    "mt_set_option": (_I32, [_I32, _I32]),
     "mt_launch_count": (ctypes.c_longlong, []),
     "mt_prof_begin": (ctypes.c_int, [_I32]),
     "mt_prof_end": (ctypes.c_int, [_I32, _V, _V, _V, _V]),

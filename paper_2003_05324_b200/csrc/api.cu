@@ -168,9 +168,24 @@ double zeta_odd(int idx) {  // covmath.py:52-66 (sum k^-s, k < 60, + Euler-Macla
 }
 }  // namespace
 
+// ------------------------------------------------------------ runtime options
+static int g_engine = MT_ENGINE_TF32X3;
+static int g_update_ctas = 0;  // 0 = all SMs
+int mt_opt_engine() { return g_engine; }
+int mt_opt_update_ctas() { return g_update_ctas; }
+
 extern "C" {
 
-int32_t mt_version(void) { return 10; }
+int32_t mt_version(void) { return 11; }
+
+/* option 0: FP32 update engine (0 FFMA SIMT, 1 tcgen05 3xTF32);
+ * option 1: CTA cap of the bulk trailing update (0 = all SMs). Returns old value. */
+int32_t mt_set_option(int32_t option, int32_t value) {
+  int old = -1;
+  if (option == 0) { old = g_engine; g_engine = value; }
+  else if (option == 1) { old = g_update_ctas; g_update_ctas = value; }
+  return old;
+}
 const char* mt_last_error(void) { return g_err; }
 
 int64_t mt_dp_tiles(int32_t p, int32_t t, int32_t mode) {
@@ -187,6 +202,10 @@ int64_t mt_sp_tiles(int32_t p, int32_t t, int32_t mode) {
 }
 int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode) {
   return (mode == MT_MODE_MP && t < p) ? 2 * (int64_t)t : 0;
+}
+
+int64_t mt_split_tiles(int32_t p, int32_t t, int32_t mode) {
+  return (mode == MT_MODE_MP && t < p) ? 4 * (int64_t)p : 0;
 }
 
 int mt_matern_prepare(double variance, double spatial_range, double smoothness, mt_matern* th) {

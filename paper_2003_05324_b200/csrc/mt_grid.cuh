@@ -23,6 +23,7 @@ struct Grid {
   float* sp;
   float* scratch;
   int64_t* status;
+  float* split;
 
   MT_HD int64_t tile_elems() const { return (int64_t)nb * nb; }
   MT_HD bool band(int i, int j) const { return (i - j) < t; }
@@ -55,6 +56,11 @@ struct Grid {
 
   // scratch ring: slot s holds [narrowed L_kk][mirrors of band panel rows k+1..k+t-1]
   MT_HD float* sdiag(int k) const { return scratch + (int64_t)(k & 1) * t * tile_elems(); }
+  // TF32 hi/lo split of FP32 operand (i, k) of panel k (tensor-core engine)
+  MT_HD float* split_hi(int i, int k) const {
+    return split + ((int64_t)(k & 1) * p + i) * 2 * tile_elems();
+  }
+  MT_HD float* split_lo(int i, int k) const { return split_hi(i, k) + tile_elems(); }
   MT_HD float* smirror(int i, int k) const { return sdiag(k) + (int64_t)(i - k) * tile_elems(); }
   // FP32 operand for tile (i,k) of panel k in an FP32 update: payload or mirror
   MT_HD const float* sp_operand(int i, int k) const {
@@ -89,6 +95,7 @@ inline Grid make_grid(const mt_tiles* g) {
   Grid r;
   r.n = g->n; r.nb = g->nb; r.p = g->p; r.t = g->t; r.mode = g->mode;
   r.dp = g->dp_pool; r.sp = g->sp_pool; r.scratch = g->scratch; r.status = g->status;
+  r.split = g->split;
   return r;
 }
 
@@ -121,3 +128,10 @@ struct ProfScope {
   }
   ~ProfScope() { mt_prof_stop(tok, st); }
 };
+
+// runtime options (api.cu): FP32 update engine and grid cap of the bulk update
+enum MtEngine { MT_ENGINE_FFMA = 0, MT_ENGINE_TF32X3 = 1 };
+int mt_opt_engine();
+int mt_opt_update_ctas();
+bool mt_tc_supported(const Grid& g);
+int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st);

@@ -1,0 +1,329 @@
+// FP32 (off-band) trailing update on the 5th-gen tensor cores: 3xTF32.
+//
+//   C_ij <- C_ij - A_ik A_jk^T      (kernels.gemm FP32 path, factor.py:273-274)
+//
+// FP32 products are emulated with three TF32 UMMAs per K-step,
+//   A B^T ~= A_lo B_hi^T + A_hi B_lo^T + A_hi B_hi^T,
+// hi = cvt.rna.tf32(x) (exactly representable in TF32), lo = x - hi (exact
+// in FP32).  The dropped A_lo B_lo term and the TF32 truncation of lo are
+// O(2^-22) relative, i.e. FP32-class accuracy (checked against the FFMA
+// kernel and the CPU reference in tests/test_gpu_tc.py).  The hi/lo split is
+// produced once per panel tile by the TRSM epilogue (Grid::split_hi/lo), so
+// the update streams both halves straight from L2 with TMA -- no per-stage
+// conversion through the LSU pipe.
+//
+// Structure (one CTA per SM, persistent over the step's 128x256 work items):
+//   warp 0      TMA producer: 16-wide K slabs of A_hi, B_hi, A_lo, B_lo
+//               (SWIZZLE_64B), 4-stage mbarrier ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128,
+//               N=256, K=8, kind::tf32), commits to mbarriers
+//   warps 2-5   epilogue: tcgen05.ld 32 columns/thread, transposed through
+//               shared memory, coalesced C -= acc in HBM; TMEM is
+//               double-buffered so it overlaps the next item's MMAs
+// Work items are ordered by output tile, so concurrently running CTAs share
+// panel tiles in L2.  Every output element is written by one CTA per step in
+// ascending k: deterministic, schedule-invariant.
+#include <cuda.h>
+
+#include "mt_grid.cuh"
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4;          // 8 KB
+constexpr int B_BYTES = BN * BK * 4;          // 16 KB
+constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 48 KB
+constexpr int NUM_THREADS = 192;
+constexpr int EPI_STRIDE = 33;                        // transpose tile, conflict-free
+constexpr int EPI_BYTES = 4 * 32 * EPI_STRIDE * 4;    // 4 warps x 32x33 floats
+constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// K-major, SWIZZLE_64B smem matrix descriptor (8-row atoms of 64 B, SBO = 512 B)
+__device__ __forceinline__ uint64_t sw64_desc(const void* p) {
+  const uint64_t a = (smem_u32(p) >> 4) & 0x3FFF;
+  return a | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) | (4ull << 61);
+}
+// kind::tf32, D f32, A/B tf32 K-major, N = 256, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+struct Work {
+  int64_t slot0;
+  int nitems;  // slots * nsub
+  int nsubm, nsubn;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc32_update_kernel(Grid g, int k, Work w, const __grid_constant__ CUtensorMap map_a,
+                       const __grid_constant__ CUtensorMap map_b) {
+  if (g.failed()) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);  // SW64 needs 512B+
+  float* epi = (float*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES + EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = g.nb;
+  const int ksteps = nb / BK;
+  const int nsub = w.nsubm * w.nsubn;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto item_ij = [&](int item, int& i, int& j, int& m0, int& n0) {
+    const int64_t slot = w.slot0 + item / nsub;
+    const int sub = item % nsub;
+    g.off_slot_ij(slot, i, j);
+    m0 = (sub / w.nsubn) * BM;
+    n0 = (sub % w.nsubn) * BN;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < w.nitems; item += gridDim.x) {
+        int i, j, m0, n0;
+        item_ij(item, i, j, m0, n0);
+        // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb
+        const int arow = ((k & 1) * g.p + i) * 2 * nb + m0;
+        const int brow = ((k & 1) * g.p + j) * 2 * nb + n0;
+        for (int ks = 0; ks < ksteps; ++ks, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          unsigned char* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(st, &map_a, &full[s], ks * BK, arow);                       // A hi
+          tma_load_2d(st + A_BYTES, &map_b, &full[s], ks * BK, brow);             // B hi
+          tma_load_2d(st + A_BYTES + B_BYTES, &map_a, &full[s], ks * BK, arow + nb);   // A lo
+          tma_load_2d(st + 2 * A_BYTES + B_BYTES, &map_b, &full[s], ks * BK, brow + nb);  // B lo
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    uint32_t it = 0, li = 0;
+    for (int item = blockIdx.x; item < w.nitems; item += gridDim.x, ++li) {
+      const uint32_t b = li & 1, aph = (li >> 1) & 1;
+      mbar_wait(&tempty[b], aph ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t dcol = tmem_base + b * BN;
+      for (int ks = 0; ks < ksteps; ++ks, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          unsigned char* st = smem + s * STAGE_BYTES;
+          const unsigned char* ahi = st;
+          const unsigned char* bhi = st + A_BYTES;
+          const unsigned char* alo = st + A_BYTES + B_BYTES;
+          const unsigned char* blo = alo + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const int off = kk * 32;  // 8 fp32 along K = 32 B inside the 64 B swizzle row
+            const uint32_t first = (ks == 0 && kk == 0) ? 0u : 1u;
+            umma_tf32(dcol, sw64_desc(alo + off), sw64_desc(bhi + off), first);
+            umma_tf32(dcol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
+            umma_tf32(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off), 1u);
+          }
+          umma_commit(&empty[s]);                          // stage free when these finish
+          if (ks == ksteps - 1) umma_commit(&tfull[b]);    // accumulator ready
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;          // TMEM lane quadrant this warp may access
+    float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
+    uint32_t li = 0;
+    for (int item = blockIdx.x; item < w.nitems; item += gridDim.x, ++li) {
+      int i, j, m0, n0;
+      item_ij(item, i, j, m0, n0);
+      const uint32_t b = li & 1, aph = (li >> 1) & 1;
+      mbar_wait(&tfull[b], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // rows q*32 .. q*32+31 of the 128x256 item; lane owns row q*32+lane in TMEM
+      float* cbase = g.stile(i, j) + (int64_t)(m0 + q * 32) * nb + n0;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr + c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // transpose the 32x32 block through shared memory (row = lane -> column = lane)
+#pragma unroll
+        for (int u = 0; u < 32; ++u) stg[lane * EPI_STRIDE + u] = __uint_as_float(v[u]);
+        __syncwarp();
+        float cv[32];
+        float* cp = cbase + c + lane;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) cv[r] = cp[(int64_t)r * nb];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) cp[(int64_t)r * nb] = cv[r] - stg[r * EPI_STRIDE + lane];
+        __syncwarp();
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+int make_map(CUtensorMap* m, const float* base, int64_t rows, int nb, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) { mt_set_error("cuTensorMapEncodeTiled unavailable"); return MT_E_CUDA; }
+  cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)(rows > 0 ? rows : 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)nb * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    mt_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return MT_E_CUDA;
+  }
+  return MT_OK;
+}
+
+int g_sm_count = 0;
+
+}  // namespace
+
+bool mt_tc_supported(const Grid& g) {
+  return g.mode == MT_MODE_MP && g.split != nullptr && g.nb % BN == 0 &&
+         (int64_t)4 * g.p * g.nb < (1ll << 31);
+}
+
+// FP32 updates of step k into off-band slots [s0, s0+scnt) via tcgen05; `ctas` caps the grid.
+int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st) {
+  if (scnt <= 0) return MT_OK;
+  CUtensorMap ma, mb;
+  const int64_t split_rows = (int64_t)4 * g.p * g.nb;  // 2 panels x p tiles x {hi, lo}
+  int rc = make_map(&ma, g.split, split_rows, g.nb, BM);
+  if (!rc) rc = make_map(&mb, g.split, split_rows, g.nb, BN);
+  if (rc) return rc;
+  Work w;
+  w.slot0 = s0;
+  w.nsubm = g.nb / BM;
+  w.nsubn = g.nb / BN;
+  w.nitems = (int)(scnt * w.nsubm * w.nsubn);
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int grid = ctas > 0 ? ctas : g_sm_count;
+  if (grid > w.nitems) grid = w.nitems;
+  const size_t smem = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  cudaFuncSetAttribute(tc32_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tc32_update_kernel<<<grid, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+  MT_LAUNCH_CHECK("tc32_update_kernel");
+  return MT_OK;
+}

@@ -97,12 +97,25 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   __syncthreads();
-  // write back (and the FP32 mirror of band rows feeding FP32 updates)
+  // write back; FP32 operands of this step's FP32 updates also get their
+  // narrowed mirror (band rows, factor.py:261-262) and, for the tensor-core
+  // engine, the TF32 hi/lo split (hi = rna(x), lo = x - hi) read by UMMA
+  const bool fp32_operand = (sizeof(T) == 4) || (M != nullptr);
+  float* SH = (g.split && fp32_operand) ? g.split_hi(i, k) : nullptr;
+  float* SL = SH ? g.split_lo(i, k) : nullptr;
   for (int e = threadIdx.x; e < nr * nb; e += kThreads) {
     int r = e / nb, c = e % nb;
     T v = X[r * ldx + c];
-    B[(int64_t)(r0 + r) * nb + c] = v;
-    if (M) M[(int64_t)(r0 + r) * nb + c] = __double2float_rn((double)v);
+    const int64_t o = (int64_t)(r0 + r) * nb + c;
+    B[o] = v;
+    const float f = __double2float_rn((double)v);
+    if (M) M[o] = f;
+    if (SH) {
+      uint32_t h;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
+      SH[o] = __uint_as_float(h);
+      SL[o] = f - __uint_as_float(h);
+    }
   }
 }
 

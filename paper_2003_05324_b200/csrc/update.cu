@@ -254,6 +254,12 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
   if (scnt > 0) {
     ProfScope ps(MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
+    if (mt_opt_engine() == MT_ENGINE_TF32X3 && mt_tc_supported(g)) {
+      // the panel-column update (jhi == jlo + 1) runs beside the bulk update:
+      // keep it narrow; the bulk update may be capped to leave SMs for the panel
+      const int ctas = (jhi == jlo + 1) ? 16 : mt_opt_update_ctas();
+      return mt_tc_update_impl(g, k, s0, scnt, ctas, st);
+    }
     if (nb % SBM == 0) {
       const int nsub = nb / SBM;
       sgemm_update_kernel<<<(unsigned)(scnt * nsub * nsub), 256, 0, st>>>(g, k, s0, nsub);

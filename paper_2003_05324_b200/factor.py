@@ -222,3 +222,19 @@ def reconstruction_error(factor, reference):
     r = ref - low @ low.T
     # absent (DST) tiles count as zero blocks of L, matching the reference
     return float(math.sqrt(float(np.sum(r * r))))
+
+
+_ENGINES = {"ffma": 0, "tf32x3": 1}
+
+
+def set_fp32_engine(name):
+    """Select the off-band (FP32) update engine: 'tf32x3' (tcgen05 3xTF32, the
+    default, used when nb is a multiple of 256) or 'ffma' (SIMT FP32).
+    Returns the previous engine name."""
+    old = _lib.load().mt_set_option(0, _ENGINES[name])
+    return {v: k for k, v in _ENGINES.items()}[old]
+
+
+def set_update_ctas(ctas):
+    """Cap the CTAs of the bulk trailing update (0 = all SMs); returns the old cap."""
+    return _lib.load().mt_set_option(1, int(ctas))

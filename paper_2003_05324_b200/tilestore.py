@@ -163,13 +163,16 @@ class TileMatrix:
         ndp = lib.mt_dp_tiles(self.p, t, mode)
         nsp = lib.mt_sp_tiles(self.p, t, mode)
         nsc = lib.mt_scratch_tiles(self.p, t, mode)
+        nsl = lib.mt_split_tiles(self.p, t, mode) if self.nb % 256 == 0 else 0
         self.dp_pool = torch.empty(max(ndp, 1) * te, dtype=torch.float64, device=dev)
         self.sp_pool = torch.empty(max(nsp, 1) * te, dtype=torch.float32, device=dev)
         self.scratch = torch.empty(max(nsc, 1) * te, dtype=torch.float32, device=dev)
+        self.split = (torch.empty(nsl * te, dtype=torch.float32, device=dev) if nsl else None)
         self.status = torch.empty(4, dtype=torch.int64, device=dev)
         self.desc = _lib.MtTiles(self.n, self.nb, self.p, t, mode, self.dp_pool.data_ptr(),
                                  self.sp_pool.data_ptr(), self.scratch.data_ptr(),
-                                 self.status.data_ptr())
+                                 self.status.data_ptr(),
+                                 self.split.data_ptr() if self.split is not None else 0)
         self.reset_status()
         self.tiles = _TileView(self)
 
@@ -341,7 +344,7 @@ class _Probe:
         self.dummy = torch.empty(1, dtype=torch.float64, device=dev)
         p = -(-n // nb)
         self.desc = _lib.MtTiles(n, nb, p, p, 0, self.dummy.data_ptr(), 0, 0,
-                                 self.status.data_ptr())
+                                 self.status.data_ptr(), 0)
 
     def read_dups(self):
         return int(self.status[2].item())
