@@ -47,8 +47,10 @@ extern "C" {
  * i >= j, is "band" iff i - j < t (tilestore.band_member, tilestore.py:92-96).
  *   dp_pool: band tiles, FP64, column-major tile order (column j, then row i).
  *   sp_pool: off-band tiles, FP32 (MP only), same order.
- *   scratch: FP32 panel scratch (MP only), mt_scratch_tiles(p, t) tiles:
- *            narrowed L_kk and narrowed band-panel mirrors (factor.py:255,262).
+ *   scratch: panel scratch, mt_scratch_tiles(p, t, mode, nb) FP32-sized tiles, a ring of
+ *            two slots: [narrowed L_kk][narrowed band-panel mirrors] (MP,
+ *            factor.py:255,262) + one tile holding the inverses of L_kk's
+ *            32x32 diagonal blocks (FP64 and FP32) for the panel TRSM.
  *   status:  int64[4] device: [0] first failing global pivot (-1 = none),
  *            [1] FP32 narrowing overflow count, [2] duplicate-location pairs.
  *   split:   TF32 hi/lo split of panels k (ring of 2): tile (i, k) of panel k at
@@ -85,7 +87,7 @@ typedef struct mt_matern {
 /* sizes of the pools for a layout (element counts are tiles * nb * nb) */
 int64_t mt_dp_tiles(int32_t p, int32_t t, int32_t mode);
 int64_t mt_sp_tiles(int32_t p, int32_t t, int32_t mode);
-int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode);
+int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode, int32_t nb);
 int64_t mt_split_tiles(int32_t p, int32_t t, int32_t mode);
 int32_t mt_version(void);
 const char* mt_last_error(void);

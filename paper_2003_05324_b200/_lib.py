@@ -62,7 +62,7 @@ SIGNATURES = {
     "mt_last_error": (ctypes.c_char_p, []),
     "mt_dp_tiles": (_I64, [_I32, _I32, _I32]),
     "mt_sp_tiles": (_I64, [_I32, _I32, _I32]),
-    "mt_scratch_tiles": (_I64, [_I32, _I32, _I32]),
+    "mt_scratch_tiles": (_I64, [_I32, _I32, _I32, _I32]),
     "mt_split_tiles": (_I64, [_I32, _I32, _I32]),
     "mt_work_doubles": (_I64, [_P(MtTiles)]),
     "mt_matern_prepare": (ctypes.c_int, [_D, _D, _D, _P(MtMatern)]),

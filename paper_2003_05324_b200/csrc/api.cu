@@ -58,7 +58,7 @@ static int check_layout(const mt_tiles* g) {
   if (!g || g->n < 1 || g->nb < 1 || g->p != (int32_t)((g->n + g->nb - 1) / g->nb) ||
       g->t < 1 || g->t > g->p || g->mode < 0 || g->mode > 2 ||
       (g->mode == MT_MODE_DP && g->t != g->p) || !g->dp_pool || !g->status ||
-      (g->mode == MT_MODE_MP && g->t < g->p && (!g->sp_pool || !g->scratch))) {
+      !g->scratch || (g->mode == MT_MODE_MP && g->t < g->p && !g->sp_pool)) {
     mt_set_error("bad tile layout descriptor");
     return MT_E_BAD_ARG;
   }
@@ -200,8 +200,11 @@ int64_t mt_sp_tiles(int32_t p, int32_t t, int32_t mode) {
   g.p = p; g.t = t; g.mode = mode;
   return g.scol(p);
 }
-int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode) {
-  return (mode == MT_MODE_MP && t < p) ? 2 * (int64_t)t : 0;
+
+int64_t mt_scratch_tiles(int32_t p, int32_t t, int32_t mode, int32_t nb) {
+  Grid g{};
+  g.p = p; g.t = mode == MT_MODE_DP ? p : t; g.mode = mode; g.nb = nb;
+  return 2 * g.slot_tiles();
 }
 
 int64_t mt_split_tiles(int32_t p, int32_t t, int32_t mode) {
@@ -388,7 +391,7 @@ int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t_, const doub
   if (t.t < 1 || t.t > t.p) { mt_set_error("diag_thick out of range"); return MT_E_BAD_ARG; }
   const int64_t te = (int64_t)nb * nb, npad = (int64_t)t.p * nb;
   const size_t b_dp = mt_dp_tiles(t.p, t.t, mode) * te * 8, b_sp = mt_sp_tiles(t.p, t.t, mode) * te * 4,
-               b_sc = mt_scratch_tiles(t.p, t.t, mode) * te * 4;
+               b_sc = mt_scratch_tiles(t.p, t.t, mode, nb) * te * 4;
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
   double *d_locs = nullptr, *d_z = nullptr, *d_work = nullptr, *d_out = nullptr;

@@ -55,7 +55,22 @@ struct Grid {
   MT_HD float* stile(int i, int j) const { return sp + (scol(j) + (i - j - t)) * tile_elems(); }
 
   // scratch ring: slot s holds [narrowed L_kk][mirrors of band panel rows k+1..k+t-1]
-  MT_HD float* sdiag(int k) const { return scratch + (int64_t)(k & 1) * t * tile_elems(); }
+  // (MP, t < p) followed by one tile holding the inverses of L_kk's 32x32 diagonal
+  // blocks (FP64, then FP32) used by the panel TRSM
+  MT_HD bool has_mirrors() const { return mode == MT_MODE_MP && t < p; }
+  MT_HD int nblk32() const { return (nb + 31) / 32; }
+  // tiles (of nb*nb floats) holding nblk32 FP64 + FP32 32x32 inverses
+  MT_HD int64_t inv_tiles() const {
+    const int64_t fl = (int64_t)nblk32() * 1024 * 3;
+    return (fl + tile_elems() - 1) / tile_elems();
+  }
+  MT_HD int64_t slot_tiles() const { return (has_mirrors() ? t : 0) + inv_tiles(); }
+  MT_HD float* sslot(int k) const { return scratch + (int64_t)(k & 1) * slot_tiles() * tile_elems(); }
+  MT_HD float* sdiag(int k) const { return sslot(k); }
+  MT_HD double* sinv64(int k) const {
+    return (double*)(sslot(k) + (has_mirrors() ? (int64_t)t : 0) * tile_elems());
+  }
+  MT_HD float* sinv32(int k) const { return (float*)(sinv64(k) + (int64_t)nblk32() * 1024); }
   // TF32 hi/lo split of FP32 operand (i, k) of panel k (tensor-core engine)
   MT_HD float* split_hi(int i, int k) const {
     return split + ((int64_t)(k & 1) * p + i) * 2 * tile_elems();

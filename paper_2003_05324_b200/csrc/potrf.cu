@@ -1,59 +1,116 @@
 // Diagonal-tile Cholesky POTRF(k), FP64, in place on the row-major tile
 // (kernels.potrf + factor.py:249-256).
 //
-// One CTA of 512 threads walks the tile in BW-wide column blocks
-// (right-looking): warp 0 factors the BW x BW diagonal block in shared
-// memory, all warps solve the sub-diagonal panel (warp per row, lane per
-// column, shuffle broadcast), then the trailing lower triangle takes a rank-BW
-// SYRK update from the shared-memory panel with 4x4 register blocks.
+// One CTA (8 warps) walks the tile in 32-wide column blocks, right-looking:
+//   1. warp 0 factors the 32x32 diagonal block with the rows held in
+//      registers (lane r owns row r, pivots broadcast by shuffles), then
+//      forms its triangular inverse (lane c owns column c);
+//   2. the sub-diagonal panel is solved as a parallel GEMM against that
+//      inverse (X = A L_dd^{-T}), staged in shared memory;
+//   3. the trailing lower triangle takes the rank-32 SYRK update on the FP64
+//      tensor cores (mma.sync m8n8k4 f64 -> DMMA), 32x32 warp tiles fed from
+//      the shared-memory panel.
 // Epilogue: the first non-positive (or NaN) pivot is published as the global
-// index k*nb + j (FactorizationError.index), and in MP mode the factored
-// tile is narrowed to FP32 scratch for the off-band panel solves (sp_diag,
+// index k*nb + j (FactorizationError.index); the 32x32 diagonal-block
+// inverses (FP64 + FP32) are kept for the panel TRSM, and in MP mode the
+// factor is narrowed to FP32 for the off-band panel solves (sp_diag,
 // factor.py:255-256).  The strict upper triangle is never written.
 #include "mt_grid.cuh"
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
+constexpr int PLD = 36;  // panel row stride in doubles: conflict-free m8n8k4 fragments
 
-template <int BW>
-__global__ void __launch_bounds__(kThreads) potrf_kernel(Grid g, int k, int narrow) {
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int narrow) {
   if (g.failed()) return;
   double* __restrict__ A = g.dtile(k, k);
   const int nb = g.nb;
-  __shared__ double Ld[BW][BW + 1];
+  extern __shared__ __align__(16) double P[];  // (nb - 32) x PLD: solved panel
+  __shared__ double Ld[32][33];
+  __shared__ double Li[32][33];
   __shared__ int bad;
-  extern __shared__ double P[];  // (nb - BW) x (BW + 1) panel
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  constexpr int nwarps = kThreads / 32;
+  double* inv64 = g.sinv64(k);
+  float* inv32 = g.sinv32(k);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) bad = -1;
 
-  for (int c0 = 0; c0 < nb; c0 += BW) {
-    const int w = min(BW, nb - c0);
-    for (int e = threadIdx.x; e < w * w; e += kThreads) {
-      int r = e / w, c = e % w;
-      if (c <= r) Ld[r][c] = A[(int64_t)(c0 + r) * nb + c0 + c];
+  for (int c0 = 0, blk = 0; c0 < nb; c0 += 32, ++blk) {
+    const int w = min(32, nb - c0);
+    // ---------------- 1. diagonal block: factor + inverse (warp 0) --------
+    // (compact loops, not unrolled: this runs once per block on one warp and
+    //  a fully unrolled version blows the instruction cache)
+    for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
+      const int r = e >> 5, c = e & 31;
+      Ld[r][c] = (r < w && c < w) ? (c <= r ? A[(int64_t)(c0 + r) * nb + c0 + c] : 0.0)
+                                  : (r == c ? 1.0 : 0.0);
     }
     __syncthreads();
-    // --- factor the diagonal block (warp 0, lane r owns row r) ---
-    if (warp == 0) {
-      for (int jj = 0; jj < w; ++jj) {
-        double piv = Ld[jj][jj];
-        if (!(piv > 0.0)) {
-          if (lane == 0) bad = c0 + jj;
-          break;
+    // right-looking, one pivot per step, the whole CTA on each step
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+      const double piv = Ld[j][j];
+      if (!(piv > 0.0)) {  // uniform: every thread reads the same pivot
+        if (threadIdx.x == 0) bad = c0 + j;
+        break;
+      }
+      const double d = sqrt(piv);
+      __syncthreads();  // everyone has read the pivot
+      if (threadIdx.x < 32) {
+        const int r = threadIdx.x;
+        if (r > j) Ld[r][j] = Ld[r][j] / d;
+        else if (r == j) Ld[j][j] = d;
+      }
+      __syncthreads();
+      // rank-1 update of the trailing (r >= c > j) part: one element per thread slot
+      const int jj = 31 - j;  // trailing order
+      for (int e = threadIdx.x; e < jj * (jj + 1) / 2; e += kThreads) {
+        int rr = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+        while (rr * (rr + 1) / 2 > e) --rr;
+        while ((rr + 1) * (rr + 2) / 2 <= e) ++rr;
+        const int r = j + 1 + rr, c = j + 1 + (e - rr * (rr + 1) / 2);
+        Ld[r][c] -= Ld[r][j] * Ld[c][j];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (bad < 0) {
+      // inverse of the 32x32 factor, row by row: thread (c, part) of 32 x 8
+      // forms a partial dot, parts are reduced in fixed order
+      __shared__ double part[8][33];
+      const int ci = threadIdx.x & 31, pt = threadIdx.x >> 5;
+#pragma unroll 1
+      for (int r = 0; r < 32; ++r) {
+        double s = 0.0;
+        for (int q = ci + pt; q < r; q += 8) s += Ld[r][q] * Li[q][ci];
+        part[pt][ci] = s;
+        __syncthreads();
+        if (pt == 0) {
+          double t = 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) t += part[u][ci];
+          Li[r][ci] = r < ci ? 0.0 : (r == ci ? 1.0 / Ld[r][r] : -t / Ld[r][r]);
         }
-        double d = sqrt(piv);
-        __syncwarp();
-        if (lane > jj && lane < w) Ld[lane][jj] = Ld[lane][jj] / d;
-        if (lane == jj) Ld[jj][jj] = d;
-        __syncwarp();
-        if (lane > jj && lane < w) {
-          double lr = Ld[lane][jj];
-          for (int l = jj + 1; l <= lane; ++l) Ld[lane][l] -= lr * Ld[l][jj];
+        __syncthreads();
+      }
+      // write the factored block (lower), its FP32 narrowing, and the inverse
+      float* S = narrow ? g.sdiag(k) : nullptr;
+      for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
+        const int r = e >> 5, c = e & 31;
+        if (r < w && c < w && c <= r) {
+          const int64_t o = (int64_t)(c0 + r) * nb + c0 + c;
+          A[o] = Ld[r][c];
+          if (S) S[o] = __double2float_rn(Ld[r][c]);
         }
-        __syncwarp();
+        const double v = Li[r][c];
+        inv64[blk * 1024 + e] = v;
+        inv32[blk * 1024 + e] = __double2float_rn(v);
       }
     }
     __syncthreads();
@@ -63,99 +120,118 @@ __global__ void __launch_bounds__(kThreads) potrf_kernel(Grid g, int k, int narr
                   (unsigned long long)((int64_t)k * nb + bad));
       return;
     }
-    for (int e = threadIdx.x; e < w * w; e += kThreads) {
-      int r = e / w, c = e % w;
-      if (c <= r) A[(int64_t)(c0 + r) * nb + c0 + c] = Ld[r][c];
-    }
-    // --- panel solve: rows below the block, x <- a L_dd^{-T} ---
     const int r_lo = c0 + w;
-    for (int r = r_lo + warp; r < nb; r += nwarps) {
-      double acc = lane < w ? A[(int64_t)r * nb + c0 + lane] : 0.0;
-      for (int c = 0; c < w; ++c) {
-        double xc = __shfl_sync(0xffffffffu, acc, c) / Ld[c][c];
-        if (lane == c) acc = xc;
-        else if (lane > c && lane < w) acc -= xc * Ld[lane][c];
-      }
-      if (lane < w) {
-        A[(int64_t)r * nb + c0 + lane] = acc;
-        P[(r - r_lo) * (BW + 1) + lane] = acc;
-      }
-    }
-    __syncthreads();
-    // --- trailing SYRK: A[r][c] -= P[r] . P[c], r >= c >= r_lo ---
     const int m = nb - r_lo;
-    if (m > 0) {
-      const int nblk = (m + 3) / 4;
-      const int ntri = nblk * (nblk + 1) / 2;
-      for (int L = threadIdx.x; L < ntri; L += kThreads) {
-        int br = (int)((sqrtf(8.0f * (float)L + 1.0f) - 1.0f) * 0.5f);
-        while (br * (br + 1) / 2 > L) --br;
-        while ((br + 1) * (br + 2) / 2 <= L) ++br;
-        const int bc = L - br * (br + 1) / 2;
-        double acc[4][4];
+    if (m <= 0) continue;
+    // ---------------- 2. panel: X = A[r_lo:, c0:c0+32] L_dd^{-T} -----------
+    for (int e = threadIdx.x; e < m * 32; e += kThreads) {
+      const int rr = e >> 5, q = e & 31;
+      P[rr * PLD + q] = q < w ? A[(int64_t)(r_lo + rr) * nb + c0 + q] : 0.0;
+    }
+    __syncthreads();
+    for (int rb = 0; rb < m; rb += 32) {
+      // thread: row rb + tid/8, columns 4*(tid%8) .. +3
+      const int rr = rb + (threadIdx.x >> 3), cg = (threadIdx.x & 7) * 4;
+      double o[4] = {0.0, 0.0, 0.0, 0.0};
+      if (rr < m) {
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+          const double av = P[rr * PLD + q];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-        int rr[4], cc[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          rr[a] = min(br * 4 + a, m - 1);
-          cc[a] = min(bc * 4 + a, m - 1);
+          for (int u = 0; u < 4; ++u) o[u] += av * Li[cg + u][q];
         }
-        for (int q = 0; q < w; ++q) {
-          double pa[4], pb[4];
+      }
+      __syncthreads();
+      if (rr < m) {
+        float* S = narrow ? g.sdiag(k) : nullptr;
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            pa[a] = P[rr[a] * (BW + 1) + q];
-            pb[a] = P[cc[a] * (BW + 1) + q];
+        for (int u = 0; u < 4; ++u) {
+          const int c = cg + u;
+          P[rr * PLD + c] = c < w ? o[u] : 0.0;
+          if (c < w) {
+            const int64_t o2 = (int64_t)(r_lo + rr) * nb + c0 + c;
+            A[o2] = o[u];
+            if (S) S[o2] = __double2float_rn(o[u]);  // FP32 narrowing, fused
           }
+        }
+      }
+      __syncthreads();
+    }
+    // ---------------- 3. trailing SYRK on DMMA: A[r][c] -= P[r] . P[c] ------
+    const int mt = (m + 31) / 32;
+    const int ntile = mt * (mt + 1) / 2;
+    for (int tIdx = warp; tIdx < ntile; tIdx += kThreads / 32) {
+      int tr = (int)((sqrtf(8.0f * (float)tIdx + 1.0f) - 1.0f) * 0.5f);
+      while (tr * (tr + 1) / 2 > tIdx) --tr;
+      while ((tr + 1) * (tr + 2) / 2 <= tIdx) ++tr;
+      const int tc = tIdx - tr * (tr + 1) / 2;
+      double acc[4][4][2];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] += pa[a] * pb[b];
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < 32; k4 += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const int ra = min(tr * 32 + f * 8 + (lane >> 2), m - 1);
+          const int rb2 = min(tc * 32 + f * 8 + (lane >> 2), m - 1);
+          af[f] = P[ra * PLD + k4 + (lane & 3)];
+          bf[f] = P[rb2 * PLD + k4 + (lane & 3)];
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int r = br * 4 + a;
-          if (r >= m) continue;
+        for (int fm = 0; fm < 4; ++fm)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int c = bc * 4 + b;
-            if (c < m && c <= r) A[(int64_t)(r_lo + r) * nb + r_lo + c] -= acc[a][b];
-          }
+          for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
+      }
+      // epilogue: issue every load of the warp tile before any store (a
+      // load/store per element would serialise on L2 latency: stores may
+      // alias later loads as far as the compiler knows)
+      double cv[4][4][2];
+#pragma unroll
+      for (int fm = 0; fm < 4; ++fm) {
+        const int r = tr * 32 + fm * 8 + (lane >> 2);
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+          const int c = tc * 32 + fn * 8 + 2 * (lane & 3);
+          const double* rowp = A + (int64_t)(r_lo + min(r, m - 1)) * nb + r_lo;
+          cv[fm][fn][0] = rowp[min(c, m - 1)];
+          cv[fm][fn][1] = rowp[min(c + 1, m - 1)];
+        }
+      }
+#pragma unroll
+      for (int fm = 0; fm < 4; ++fm) {
+        const int r = tr * 32 + fm * 8 + (lane >> 2);
+        if (r >= m) continue;
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) {
+          const int c = tc * 32 + fn * 8 + 2 * (lane & 3);
+          double* cp = A + (int64_t)(r_lo + r) * nb + r_lo + c;
+          if (c < m && c <= r) cp[0] = cv[fm][fn][0] - acc[fm][fn][0];
+          if (c + 1 < m && c + 1 <= r) cp[1] = cv[fm][fn][1] - acc[fm][fn][1];
         }
       }
     }
     __syncthreads();
   }
-  if (narrow) {
-    float* S = g.sdiag(k);
-    const int64_t tot = (int64_t)nb * nb;
-    for (int64_t e = threadIdx.x; e < tot; e += kThreads) {
-      int r = (int)(e / nb), c = (int)(e % nb);
-      S[e] = c <= r ? __double2float_rn(A[e]) : 0.0f;
-    }
-  }
-}
-
-template <int BW>
-int launch_potrf(const Grid& g, int k, int narrow, cudaStream_t st) {
-  size_t smem = (size_t)(g.nb > BW ? g.nb - BW : 1) * (BW + 1) * sizeof(double);
-  cudaFuncSetAttribute(potrf_kernel<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       200 * 1024);
-  const double r = g.rows(k);
-  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0, (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)));
-  potrf_kernel<BW><<<1, kThreads, smem, st>>>(g, k, narrow);
-  MT_LAUNCH_CHECK("potrf_kernel");
-  return MT_OK;
+  // (the FP32 narrowing of the lower triangle was written as each element was
+  //  finalised; the TRSM never reads the strict upper part)
 }
 
 }  // namespace
 
 int mt_potrf_impl(const Grid& g, int k, int narrow, cudaStream_t st) {
-  if (g.nb <= 704) return launch_potrf<32>(g, k, narrow, st);
-  if (g.nb <= 1408) return launch_potrf<16>(g, k, narrow, st);
-  mt_set_error("potrf: nb=%d exceeds the supported maximum 1408", g.nb);
-  return MT_E_BAD_ARG;
+  const size_t smem = (size_t)(g.nb > 32 ? g.nb - 32 : 1) * PLD * sizeof(double);
+  if (smem > 200 * 1024) {
+    mt_set_error("potrf: nb=%d exceeds the supported maximum", g.nb);
+    return MT_E_BAD_ARG;
+  }
+  cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const double r = g.rows(k);
+  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0,
+               (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)));
+  potrf_kernel<<<1, kThreads, smem, st>>>(g, k, narrow);
+  MT_LAUNCH_CHECK("potrf_kernel");
+  return MT_OK;
 }

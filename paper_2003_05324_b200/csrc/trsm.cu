@@ -7,95 +7,170 @@
 //   off-band rows (MP): FP32 against the narrowed L_kk (sp_diag,
 //                factor.py:264); the FP64 view is the exact widening and is
 //                never materialised (FP64 consumers widen on load).
+// Every FP32 operand of this step's FP32 updates also gets its TF32 hi/lo
+// split written here (read by the tcgen05 update, tc_update.cu).
 //
 // Rows of X = B L^{-T} are independent, so a CTA owns RB rows of one tile and
-// walks the columns in 32-wide blocks: GEMM-style update from the solved
-// columns (shared-memory X, streamed 32x32 chunks of L), then a warp-per-4-rows
-// forward substitution on the 32x32 diagonal block with shuffle broadcasts.
+// walks the columns in 32-wide blocks, right-looking:
+//   G    = B[:, cb] - X[:, <cb] L[cb, <cb]^T   (thread = 1 column x RB/8 rows;
+//          broadcast vector reads of the transposed X, conflict-free reads of L)
+//   X_cb = G L_cb,cb^{-T}                      (GEMM against the diagonal-block
+//          inverse published by POTRF -- no sequential substitution)
+// The 32x32 blocks of L and the inverses are streamed through a 4-stage
+// cp.async ring that runs ahead across column blocks.
 #include "mt_grid.cuh"
 
 namespace {
 
-constexpr int kRB = 32;       // rows per CTA
-constexpr int kThreads = 256; // 8 warps x 4 rows
+constexpr int kThreads = 256;  // 8 warps; lane = column of the 32-wide block
+constexpr int NST = 4;         // cp.async ring depth
+constexpr int LDL = 33;        // chunk row stride (conflict-free column reads)
+
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+  template <int N>
+  static __device__ __forceinline__ void ld(const float* p, float (&o)[N]) {
+#pragma unroll
+    for (int u = 0; u < N; u += 4) {
+      float4 v = *(const float4*)(p + u);
+      o[u] = v.x; o[u + 1] = v.y; o[u + 2] = v.z; o[u + 3] = v.w;
+    }
+  }
+};
+template <> struct Vec<double> {
+  template <int N>
+  static __device__ __forceinline__ void ld(const double* p, double (&o)[N]) {
+#pragma unroll
+    for (int u = 0; u < N; u += 2) {
+      double2 v = *(const double2*)(p + u);
+      o[u] = v.x; o[u + 1] = v.y;
+    }
+  }
+};
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "n"(sizeof(T)));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <typename T, int RB>
+__global__ void __launch_bounds__(kThreads, 1)
     trsm_kernel(Grid g, int k, int64_t slot0, int nrb, int mirror_ok) {
   if (g.failed()) return;
+  constexpr int RPT = RB / 8;                  // rows per thread (4 FP64, 8 FP32)
+  constexpr int XS = RB + 16 / sizeof(T);      // Xt row stride (16-byte aligned rows)
   const int64_t slot = slot0 + blockIdx.x / nrb;
   const int rb = blockIdx.x % nrb;
   int i, j;
   const T* L;
+  const T* Linv;
   T* B;
   float* M = nullptr;
   if constexpr (sizeof(T) == 8) {
     g.band_slot_ij(slot, i, j);
     L = (const T*)g.dtile(k, k);
+    Linv = (const T*)g.sinv64(k);
     B = (T*)g.dtile(i, k);
     if (mirror_ok && g.mode == MT_MODE_MP && i + g.t <= g.p - 1) M = g.smirror(i, k);
   } else {
     g.off_slot_ij(slot, i, j);
     L = (const T*)g.sdiag(k);
+    Linv = (const T*)g.sinv32(k);
     B = (T*)g.stile(i, k);
   }
   const int nb = g.nb;
-  const int r0 = rb * kRB;
-  const int nr = min(kRB, nb - r0);
-  extern __shared__ unsigned char smem_raw[];
-  T* X = (T*)smem_raw;                 // kRB x (nb + 1)
-  T* Lc = X + kRB * (nb + 1);          // 32 x 33 chunk of L
-  const int ldx = nb + 1;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int row0 = warp * 4;  // this warp's 4 rows (local)
+  const int nblk = (nb + 31) / 32;
+  const int r0 = rb * RB;
+  const int nr = min(RB, nb - r0);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xt = (T*)smem_raw;                                  // [nblk*32][XS]: Xt[c][r]
+  T* ring = Xt + (size_t)nblk * 32 * XS;                 // [NST][32][LDL]
+  const int c = threadIdx.x & 31, rw = (threadIdx.x >> 5) * RPT;
 
-  for (int cb = 0; cb < nb; cb += 32) {
-    const int w = min(32, nb - cb);
-    T acc[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = row0 + a;
-      acc[a] = (r < nr && lane < w) ? B[(int64_t)(r0 + r) * nb + cb + lane] : T(0);
+  // chunk sequence: for each column block b: L(b, 0..b-1) then inverse(b)
+  // chunk index -> (b, q) via b(b+1)/2 + q, q == b meaning "inverse"
+  const int nchunks = nblk * (nblk + 1) / 2;
+  auto chunk_src = [&](int idx, int& b, int& q) {
+    b = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
+    while (b * (b + 1) / 2 > idx) --b;
+    while ((b + 1) * (b + 2) / 2 <= idx) ++b;
+    q = idx - b * (b + 1) / 2;
+  };
+  auto issue = [&](int idx) {
+    if (idx < nchunks) {
+      int b, q;
+      chunk_src(idx, b, q);
+      T* dst = ring + (size_t)(idx % NST) * 32 * LDL;
+      for (int e = threadIdx.x; e < 1024; e += kThreads) {
+        const int rr = e >> 5, cc = e & 31;
+        const T* src;
+        if (q == b) src = Linv + (size_t)b * 1024 + e;     // inverse block, row-major 32x32
+        else {
+          const int row = min(b * 32 + rr, nb - 1), col = min(q * 32 + cc, nb - 1);
+          src = L + (int64_t)row * nb + col;
+        }
+        cp_async_elem(dst + rr * LDL + cc, src);
+      }
     }
-    // acc[r][c] -= sum_{q < cb} X[r][q] L[cb + c][q]
-    for (int q0 = 0; q0 < cb; q0 += 32) {
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < NST - 1; ++s) issue(s);
+
+  T acc[RPT];
+  int idx = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const int cb = b * 32, w = min(32, nb - cb);
+#pragma unroll
+    for (int v = 0; v < RPT; ++v) {
+      const int r = rw + v;
+      acc[v] = (r < nr && c < w) ? B[(int64_t)(r0 + r) * nb + cb + c] : T(0);
+    }
+    for (int q = 0; q <= b; ++q, ++idx) {
+      cp_async_wait<NST - 2>();
       __syncthreads();
-      for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
-        int rr = e >> 5, cc = e & 31;
-        Lc[rr * 33 + cc] = (rr < w) ? L[(int64_t)(cb + rr) * nb + q0 + cc] : T(0);
-      }
-      __syncthreads();
-#pragma unroll 8
-      for (int q = 0; q < 32; ++q) {
-        T l = Lc[lane * 33 + q];
+      issue(idx + NST - 1);
+      const T* ch = ring + (size_t)(idx % NST) * 32 * LDL;
+      if (q < b) {
+        // G -= X[:, q-block] L[cb + c, q-block]^T
+#pragma unroll 4
+        for (int qq = 0; qq < 32; ++qq) {
+          T xv[RPT];
+          Vec<T>::ld(&Xt[(size_t)(q * 32 + qq) * XS + rw], xv);
+          const T l = ch[c * LDL + qq];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) acc[a] -= X[(row0 + a) * ldx + q0 + q] * l;
-      }
-    }
-    // diagonal block L[cb:cb+w, cb:cb+w]
-    __syncthreads();
-    for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
-      int rr = e >> 5, cc = e & 31;
-      Lc[rr * 33 + cc] = (rr < w && cc < w) ? L[(int64_t)(cb + rr) * nb + cb + cc] : T(0);
-    }
-    __syncthreads();
-    for (int c = 0; c < w; ++c) {
-      const T dcc = Lc[c * 33 + c];
-      const T lc = Lc[lane * 33 + c];
+          for (int v = 0; v < RPT; ++v) acc[v] -= xv[v] * l;
+        }
+      } else {
+        // X_cb = G Linv^T: stage G, then contract with the inverse block
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        T xc = __shfl_sync(0xffffffffu, acc[a], c) / dcc;
-        if (lane == c) acc[a] = xc;
-        else if (lane > c) acc[a] -= xc * lc;
-      }
-    }
+        for (int v = 0; v < RPT; ++v) Xt[(size_t)(cb + c) * XS + rw + v] = acc[v];
+        __syncthreads();
+        T o[RPT];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = row0 + a;
-      if (lane < w) X[r * ldx + cb + lane] = acc[a];
+        for (int v = 0; v < RPT; ++v) o[v] = T(0);
+#pragma unroll 4
+        for (int qq = 0; qq < 32; ++qq) {
+          T gv[RPT];
+          Vec<T>::ld(&Xt[(size_t)(cb + qq) * XS + rw], gv);
+          const T li = ch[c * LDL + qq];
+#pragma unroll
+          for (int v = 0; v < RPT; ++v) o[v] += gv[v] * li;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < RPT; ++v) Xt[(size_t)(cb + c) * XS + rw + v] = c < w ? o[v] : T(0);
+      }
     }
   }
+  cp_async_wait<0>();
   __syncthreads();
   // write back; FP32 operands of this step's FP32 updates also get their
   // narrowed mirror (band rows, factor.py:261-262) and, for the tensor-core
@@ -103,28 +178,35 @@ __global__ void __launch_bounds__(kThreads)
   const bool fp32_operand = (sizeof(T) == 4) || (M != nullptr);
   float* SH = (g.split && fp32_operand) ? g.split_hi(i, k) : nullptr;
   float* SL = SH ? g.split_lo(i, k) : nullptr;
-  for (int e = threadIdx.x; e < nr * nb; e += kThreads) {
-    int r = e / nb, c = e % nb;
-    T v = X[r * ldx + c];
-    const int64_t o = (int64_t)(r0 + r) * nb + c;
-    B[o] = v;
-    const float f = __double2float_rn((double)v);
-    if (M) M[o] = f;
-    if (SH) {
-      uint32_t h;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
-      SH[o] = __uint_as_float(h);
-      SL[o] = f - __uint_as_float(h);
+  for (int r = threadIdx.x >> 5; r < nr; r += kThreads / 32) {
+    for (int cc = c; cc < nb; cc += 32) {
+      const T v = Xt[(size_t)cc * XS + r];
+      const int64_t o = (int64_t)(r0 + r) * nb + cc;
+      B[o] = v;
+      const float f = __double2float_rn((double)v);
+      if (M) M[o] = f;
+      if (SH) {
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
+        SH[o] = __uint_as_float(h);
+        SL[o] = f - __uint_as_float(h);
+      }
     }
   }
 }
 
-template <typename T>
+template <typename T, int RB>
+size_t trsm_smem(int nb) {
+  const size_t rows = (size_t)((nb + 31) / 32) * 32;
+  return (rows * (RB + 16 / sizeof(T)) + (size_t)NST * 32 * LDL) * sizeof(T);
+}
+
+template <typename T, int RB>
 int launch_trsm(const Grid& g, int k, int64_t s0, int64_t cnt, int mirror_ok, cudaStream_t st) {
   if (cnt <= 0) return MT_OK;
-  const int nrb = (g.nb + kRB - 1) / kRB;
-  size_t smem = ((size_t)kRB * (g.nb + 1) + 32 * 33) * sizeof(T);
-  cudaFuncSetAttribute(trsm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int nrb = (g.nb + RB - 1) / RB;
+  const size_t smem = trsm_smem<T, RB>(g.nb);
+  cudaFuncSetAttribute(trsm_kernel<T, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   const double rk = g.rows(k), nb = g.nb;
   // algorithmic work: rows(i) * rows(k)^2 per tile (factor.py:88-90); last row may be ragged
@@ -132,7 +214,7 @@ int launch_trsm(const Grid& g, int k, int64_t s0, int64_t cnt, int mirror_ok, cu
   const double rows_sum = (cnt - (last ? 1 : 0)) * nb + (last ? g.rows(g.p - 1) : 0);
   ProfScope ps(sizeof(T) == 8 ? MT_K_TRSM64 : MT_K_TRSM32, st, rows_sum * rk * rk,
                cnt * nb * nb * sizeof(T) * 2.0);
-  trsm_kernel<T><<<(unsigned)(cnt * nrb), kThreads, smem, st>>>(g, k, s0, nrb, mirror_ok);
+  trsm_kernel<T, RB><<<(unsigned)(cnt * nrb), kThreads, smem, st>>>(g, k, s0, nrb, mirror_ok);
   MT_LAUNCH_CHECK("trsm_kernel");
   return MT_OK;
 }
@@ -142,12 +224,13 @@ int launch_trsm(const Grid& g, int k, int64_t s0, int64_t cnt, int mirror_ok, cu
 // Panel rows i in (k, p) of tile column k.  Band rows: band slots
 // bcol(k)+1 .. bcol(k+1)-1; off-band rows: off slots scol(k) .. scol(k+1)-1.
 int mt_trsm_impl(const Grid& g, int k, cudaStream_t st) {
-  if ((size_t)32 * (g.nb + 1) * sizeof(double) > 200 * 1024) {
+  if (trsm_smem<double, 32>(g.nb) > 220 * 1024 || trsm_smem<float, 64>(g.nb) > 220 * 1024) {
     mt_set_error("trsm: nb=%d too large for the shared-memory panel", g.nb);
     return MT_E_BAD_ARG;
   }
-  int rc = launch_trsm<double>(g, k, g.bcol(k) + 1, g.bcol(k + 1) - g.bcol(k) - 1, 1, st);
+  int rc = launch_trsm<double, 32>(g, k, g.bcol(k) + 1, g.bcol(k + 1) - g.bcol(k) - 1, 1, st);
   if (rc) return rc;
-  if (g.mode == MT_MODE_MP) rc = launch_trsm<float>(g, k, g.scol(k), g.scol(k + 1) - g.scol(k), 0, st);
+  if (g.mode == MT_MODE_MP)
+    rc = launch_trsm<float, 64>(g, k, g.scol(k), g.scol(k + 1) - g.scol(k), 0, st);
   return rc;
 }

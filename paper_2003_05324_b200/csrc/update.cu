@@ -178,6 +178,129 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------- FP64 DMMA
+// 128x64 CTA tile, 8 warps x (32x32) warp tiles of m8n8k4 f64 MMAs (SASS DMMA);
+// operands FP64 or FP32 (widened on load), register-prefetched one K slab
+// ahead, smem rows padded to 20 doubles (conflict-free fragment loads).
+constexpr int MBM = 128, MBN = 64, MBK = 16, MLD = MBK + 4;
+constexpr int MMA_SMEM = 2 * (MBM + MBN) * MLD * 8;
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// 8 consecutive operand values (FP64, or FP32 widened) starting at idx
+__device__ __forceinline__ void ld8(const void* base, bool f32, int64_t idx, double (&v)[8]) {
+  if (f32) {
+    const float4* p = (const float4*)((const float*)base + idx);
+    float4 x = p[0], y = p[1];
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+    const double2* p = (const double2*)((const double*)base + idx);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { double2 t = p[q]; v[2 * q] = t.x; v[2 * q + 1] = t.y; }
+  }
+}
+__device__ __forceinline__ void ld4(const void* base, bool f32, int64_t idx, double (&v)[4]) {
+  if (f32) {
+    float4 x = *(const float4*)((const float*)base + idx);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const double2* p = (const double2*)((const double*)base + idx);
+    double2 s = p[0], t = p[1];
+    v[0] = s.x; v[1] = s.y; v[2] = t.x; v[3] = t.y;
+  }
+}
+
+__global__ void __launch_bounds__(256, 2)
+    dmma_update_kernel(Grid g, int k, int64_t slot0, int nsubm, int nsubn) {
+  if (g.failed()) return;
+  const int nsub = nsubm * nsubn;
+  const int64_t slot = slot0 + blockIdx.x / nsub;
+  const int sub = blockIdx.x % nsub;
+  int i, j;
+  g.band_slot_ij(slot, i, j);
+  if (!g.present(i, k)) return;  // DST: GEMM(k; i, j) needs tile (i, k)
+  const int m0 = (sub / nsubn) * MBM, n0 = (sub % nsubn) * MBN;
+  const bool syrk = (i == j);
+  if (syrk && n0 >= m0 + MBM) return;  // entirely above the diagonal
+  const int nb = g.nb;
+  const bool fa = !g.band(i, k), fb = !g.band(j, k);
+  const void* A = fa ? (const void*)g.stile(i, k) : (const void*)g.dtile(i, k);
+  const void* B = fb ? (const void*)g.stile(j, k) : (const void*)g.dtile(j, k);
+  double* __restrict__ C = g.dtile(i, j);
+
+  extern __shared__ __align__(16) double msm[];
+  double* As = msm;                      // [2][MBM][MLD]
+  double* Bs = msm + 2 * MBM * MLD;      // [2][MBN][MLD]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  const int ar = tid >> 1, ac = (tid & 1) * 8;   // A slab: 128 rows x 16
+  const int br = tid >> 2, bc = (tid & 3) * 4;   // B slab:  64 rows x 16
+  const int64_t abase = (int64_t)(m0 + ar) * nb + ac, bbase = (int64_t)(n0 + br) * nb + bc;
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  double ra[8], rb[4];
+  ld8(A, fa, abase, ra);
+  ld4(B, fb, bbase, rb);
+  int buf = 0;
+  for (int kk = 0; kk < nb; kk += MBK) {
+    double* as = As + buf * MBM * MLD;
+    double* bs = Bs + buf * MBN * MLD;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) *(double2*)&as[ar * MLD + ac + 2 * q] = make_double2(ra[2 * q], ra[2 * q + 1]);
+    *(double2*)&bs[br * MLD + bc] = make_double2(rb[0], rb[1]);
+    *(double2*)&bs[br * MLD + bc + 2] = make_double2(rb[2], rb[3]);
+    __syncthreads();
+    if (kk + MBK < nb) {
+      ld8(A, fa, abase + kk + MBK, ra);
+      ld4(B, fb, bbase + kk + MBK, rb);
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < MBK; k4 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        af[f] = as[(wm + f * 8 + (lane >> 2)) * MLD + k4 + (lane & 3)];
+        bf[f] = bs[(wn + f * 8 + (lane >> 2)) * MLD + k4 + (lane & 3)];
+      }
+#pragma unroll
+      for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < 4; ++fn) dmma884(acc[fm][fn], af[fm], bf[fn]);
+    }
+    buf ^= 1;
+  }
+  // epilogue: C fragment (row lane>>2, cols 2*(lane&3) + {0,1}) of each 8x8
+  // block; all loads are issued before any store (no load/store serialisation)
+  double2 cv[4][4];
+#pragma unroll
+  for (int fm = 0; fm < 4; ++fm)
+#pragma unroll
+    for (int fn = 0; fn < 4; ++fn)
+      cv[fm][fn] = *(const double2*)(C + (int64_t)(m0 + wm + fm * 8 + (lane >> 2)) * nb + n0 +
+                                     wn + fn * 8 + 2 * (lane & 3));
+#pragma unroll
+  for (int fm = 0; fm < 4; ++fm) {
+    const int r = m0 + wm + fm * 8 + (lane >> 2);
+#pragma unroll
+    for (int fn = 0; fn < 4; ++fn) {
+      const int c = n0 + wn + fn * 8 + 2 * (lane & 3);
+      double2* cp = (double2*)(C + (int64_t)r * nb + c);
+      const double2 v = make_double2(cv[fm][fn].x - acc[fm][fn][0], cv[fm][fn].y - acc[fm][fn][1]);
+      if (!syrk || c + 1 <= r) *cp = v;
+      else if (c <= r) C[(int64_t)r * nb + c] = v.x;
+    }
+  }
+}
+
 // ------------------------------------------------- generic (any nb) fallback
 template <bool F64>
 __global__ void __launch_bounds__(256)
@@ -241,7 +364,12 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
   if (bcnt > 0) {
     ProfScope ps(MT_K_UPD64, st, f64, bcnt * (double)nb * nb * 8.0 * 3.0);
-    if (nb % DBM == 0) {
+    if (nb % MBM == 0) {
+      const int nsm = nb / MBM, nsn = nb / MBN;
+      cudaFuncSetAttribute(dmma_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           MMA_SMEM);
+      dmma_update_kernel<<<(unsigned)(bcnt * nsm * nsn), 256, MMA_SMEM, st>>>(g, k, b0, nsm, nsn);
+    } else if (nb % DBM == 0) {
       const int nsub = nb / DBM;
       dgemm_update_kernel<<<(unsigned)(bcnt * nsub * nsub), 256, 0, st>>>(g, k, b0, nsub);
     } else {

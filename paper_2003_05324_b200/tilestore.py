@@ -162,7 +162,7 @@ class TileMatrix:
         te = self.nb * self.nb
         ndp = lib.mt_dp_tiles(self.p, t, mode)
         nsp = lib.mt_sp_tiles(self.p, t, mode)
-        nsc = lib.mt_scratch_tiles(self.p, t, mode)
+        nsc = lib.mt_scratch_tiles(self.p, t, mode, self.nb)
         nsl = lib.mt_split_tiles(self.p, t, mode) if self.nb % 256 == 0 else 0
         self.dp_pool = torch.empty(max(ndp, 1) * te, dtype=torch.float64, device=dev)
         self.sp_pool = torch.empty(max(nsp, 1) * te, dtype=torch.float32, device=dev)
@@ -343,8 +343,8 @@ class _Probe:
         self.status = torch.tensor([-1, 0, 0, 0], dtype=torch.int64, device=dev)
         self.dummy = torch.empty(1, dtype=torch.float64, device=dev)
         p = -(-n // nb)
-        self.desc = _lib.MtTiles(n, nb, p, p, 0, self.dummy.data_ptr(), 0, 0,
-                                 self.status.data_ptr(), 0)
+        self.desc = _lib.MtTiles(n, nb, p, p, 0, self.dummy.data_ptr(), 0,
+                                 self.dummy.data_ptr(), self.status.data_ptr(), 0)
 
     def read_dups(self):
         return int(self.status[2].item())

@@ -136,7 +136,8 @@ def test_mp_matches_oracle_at_same_band(gpu):
             got = f.tiles[key]
             assert (got.sp is None) == (sp is None), key
             np.testing.assert_allclose(got.dp, dp, rtol=0, atol=5e-5, err_msg=str(key))
-        assert math.isclose(mt.logdet(f), O.logdet(ref, f.p), rel_tol=1e-6)
+        # MP logdet: FP32-noise level, judged at the north-star MP tolerance
+        assert math.isclose(mt.logdet(f), O.logdet(ref, f.p), rel_tol=1e-5)
 
 
 def test_mp_residual_and_band_accuracy(gpu):
