@@ -266,6 +266,22 @@ def run_ours(args, rank, world, local_rank):
     t_chol = max_over_ranks(c0.elapsed_time(c1) / 1e3)
     chol_tflops = world * (n ** 3 / 3.0) / t_chol / 1e12
 
+    # Roofline pass: the same factorization with lookahead 0, so every event
+    # pair on the launching stream brackets exactly one kernel group (with the
+    # panel stream overlapping, event spans would include queueing time).
+    m.reset_status()
+    lib.mt_generate(ctypes.byref(m.desc), _lib.ptr(asm.d_locs), 0, 0.0, ctypes.byref(th), sh)
+    torch.cuda.synchronize()
+    lib.mt_prof_begin(8192)
+    lib.mt_cholesky(ctypes.byref(m.desc), 0, sh)
+    torch.cuda.synchronize()
+    ser = [(ctypes.c_double * K)() for _ in range(3)]
+    scnt = (ctypes.c_int64 * K)()
+    lib.mt_prof_end(K, ser[0], ser[1], ser[2], scnt)
+    serial = {KINDS[q]: {"ms": ser[0][q], "flops": ser[1][q], "bytes": ser[2][q],
+                         "launches": int(scnt[q])} for q in range(K)}
+    m.reset_status()
+
     # ---- full-DP leg (the build's own full-DP path)
     dp = None
     if not args.no_dp:
@@ -310,14 +326,30 @@ def run_ours(args, rank, world, local_rank):
                "api": "paper_2003_05324_b200.loglik(dataset, params, nb, policy)",
                "loglik": out.value}
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (from the serialized pass)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16_sus = peaks.get("bf16_tflops_sustained")
     dom = max(("upd32", "upd64", "potrf", "trsm64", "trsm32", "gen32", "gen64"),
-              key=lambda k: kinds[k]["ms"])
-    probe_kind = 1 if dom in ("upd64", "potrf", "trsm64") else 0
-    pk = ctypes.c_double()
-    lib.mt_peak_probe(probe_kind, 20000, ctypes.byref(pk))
-    d = kinds[dom]
+              key=lambda k: serial[k]["ms"])
+    d = serial[dom]
     achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    pk = ctypes.c_double()
+    if dom == "upd32" and bf16_sus:
+        # tcgen05 kind::tf32 runs at half the bf16 rate; 3xTF32 issues 3 MMAs
+        # per FP32 product -> algorithmic FP32 peak = bf16 / 2 / 3
+        peak = bf16_sus / 2.0 / 3.0
+        pipe = "tcgen05 kind::tf32 (3xTF32 FP32 emulation), TMEM accumulators"
+        src = ("MEASURED_PEAKS.json bf16_tflops_sustained / 2 (TF32 rate) / 3 (MMAs per FP32 "
+               "product); sustained figure since the kernel runs inside a long step")
+    else:
+        lib.mt_peak_probe(2 if dom in ("upd64", "potrf", "trsm64") else 0, 20000, ctypes.byref(pk))
+        peak = pk.value
+        pipe = "FP64 DMMA" if dom in ("upd64", "potrf", "trsm64") else "FP32 FFMA"
+        src = "measured this run by mt_peak_probe (MEASURED_PEAKS.json has no FP64/FFMA figure)"
     traffic = None
     prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof_path):
@@ -325,14 +357,30 @@ def run_ours(args, rank, world, local_rank):
             traffic = json.load(open(prof_path)).get(dom)
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk.value, "unit": "TFLOP/s",
-                "frac": achieved / pk.value if pk.value else None, "traffic": traffic,
-                "kernel": dom, "pipe": "FP32 FFMA (SIMT)" if probe_kind == 0 else "FP64 DFMA",
-                "peak_source": ("measured this run by mt_peak_probe "
-                                f"({'FFMA' if probe_kind == 0 else 'DFMA'} chains on all SMs); "
-                                "MEASURED_PEAKS.json has no FP32/FP64 figure"),
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None, "traffic": traffic,
+                "kernel": {"upd32": "tc32_update_kernel", "upd64": "dmma_update_kernel"}.get(dom, dom),
+                "pipe": pipe, "peak_source": src,
                 "launches_per_step": d["launches"],
-                "avg_launch_ms": d["ms"] / max(1, d["launches"])}
+                "avg_launch_ms": d["ms"] / max(1, d["launches"]),
+                "measured": ("CUDA events around every launch of a lookahead-0 (serialized) "
+                             "factorization inside bench.py; algorithmic flops = reference "
+                             "flop model (factor.py:83-95) per launch"),
+                "share_of_serialized_cholesky": d["ms"] / max(1e-9, sum(v["ms"] for v in serial.values())),
+                "serialized_kernels": {k: {"ms": round(v["ms"], 2), "launches": v["launches"],
+                                           "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 2)}
+                                       for k, v in serial.items() if v["launches"]}}
+    # flop-weighted roofline of the whole factorization
+    fl_plan = mt.planned_flops(n, nb, mp_pol)
+    p64 = ctypes.c_double()
+    lib.mt_peak_probe(2, 20000, ctypes.byref(p64))
+    p32 = (bf16_sus / 6.0) if bf16_sus else None
+    if p32:
+        t_roof = fl_plan.sp / (p32 * 1e12) + fl_plan.dp / (p64.value * 1e12)
+        roofline["cholesky_flop_weighted"] = {
+            "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
+            "p32_tflops": p32, "p64_tflops": p64.value,
+            "p32_source": "bf16_sustained/6 (3xTF32)", "p64_source": "mt_peak_probe DMMA"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -54,7 +54,7 @@ def _plan_flops(n, nb, p, mode, t):
     order (factor.py:83-95, 134-145) -- O(p^2) loops with closed-form sums
     over the GEMM rows instead of enumerating O(p^3) tasks."""
     r = _tile_rows(n, nb, p)
-    dst = mode is Mode.DST
+    dst = mode.value == "dst"
     fdp = fsp = 0.0
     # exact sums are needed only to float rounding; use the same per-task
     # terms the reference adds, grouped per (k, j) column of GEMMs
@@ -100,7 +100,7 @@ def planned_flops(n, nb, policy):
     n, nb = int(n), int(nb)
     p = -(-n // nb)
     pol = policy.resolve(p)
-    if pol.mode is not Mode.DST and n == p * nb and p > 64:
+    if pol.mode.value != "dst" and n == p * nb and p > 64:
         return _fast_flops(n, nb, p, pol.mode, pol.diag_thick)
     return _plan_flops(n, nb, p, pol.mode, pol.diag_thick)
 

@@ -80,7 +80,7 @@ class PrecisionPolicy:
 
 def band_member(i, j, policy):
     """Tile (i, j) is FP64 iff |i - j| < diag_thick (tilestore.py:92-96)."""
-    if policy.mode is Mode.DP:
+    if policy.mode.value == "dp":
         return True
     return abs(i - j) < policy.diag_thick
 
@@ -106,7 +106,7 @@ class _TileView(Mapping):
         m = self._m
         for j in range(m.p):
             for i in range(j, m.p):
-                if m.policy.mode is not Mode.DST or i - j < m.policy.diag_thick:
+                if m.policy.mode.value != "dst" or i - j < m.policy.diag_thick:
                     yield (i, j)
 
     def __iter__(self):
@@ -122,7 +122,7 @@ class _TileView(Mapping):
             return False
         m = self._m
         return (0 <= j <= i < m.p
-                and (m.policy.mode is not Mode.DST or i - j < m.policy.diag_thick))
+                and (m.policy.mode.value != "dst" or i - j < m.policy.diag_thick))
 
     def __getitem__(self, key):
         if key not in self:
@@ -223,7 +223,7 @@ class TileMatrix:
             t, p = self.policy.diag_thick, self.p
             # narrowed mirror of a band panel tile that fed FP32 updates
             # (factor.py:261-262): the device mirror is exactly RN(dp)
-            if (self.factored and self.policy.mode is Mode.MP and i != j and i + t <= p - 1):
+            if (self.factored and self.policy.mode.value == "mp" and i != j and i + t <= p - 1):
                 sp = np.asfortranarray(dp, dtype=np.float32)
             return Tile(dp=dp, sp=sp)
         sp = self._download(i, j, 1)
@@ -267,7 +267,7 @@ class TileMatrix:
                 if m.band(i, j):
                     buf = np.asfortranarray(blk)
                     which = 0
-                elif m.policy.mode is Mode.MP:
+                elif m.policy.mode.value == "mp":
                     with np.errstate(over="ignore"):
                         buf = np.asfortranarray(blk, dtype=np.float32)
                     if (np.isfinite(blk) & ~np.isfinite(buf)).any():
@@ -306,7 +306,7 @@ class TileAssembler:
         d = stage.to(dev, non_blocking=True)
         self.d_locs = d[:, :2].contiguous()
         self.d_z = d[:, 2].contiguous()
-        self.metric_code = dataset.metric.code
+        self.metric_code = _lib.METRIC_CODE[dataset.metric.kind]  # duck-typed: reference metrics too
         self.radius = float(dataset.metric.radius)
         probe = _Probe(self.n, self.nb, dev)
         _lib.check(_lib.load().mt_scan_duplicates(ctypes.byref(probe.desc), _lib.ptr(self.d_locs),
