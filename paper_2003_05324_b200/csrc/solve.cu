@@ -85,13 +85,21 @@ __global__ void __launch_bounds__(512) trsv_fwd_diag_kernel(Grid g, int i, doubl
         __syncthreads();
       }
       if (warp == 0) {
+        // stage the 32x32 diagonal block: lane r keeps row r in registers,
+        // so the serial substitution never waits on global memory
+        double lr[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          lr[q] = (lane < w && q < w) ? L[(int64_t)(cb + lane) * nb + cb + q] : 1.0;
         double acc = lane < w ? ys[cb + lane] : 0.0;
-        const double lrow = 0.0;
-        (void)lrow;
-        for (int q = 0; q < w; ++q) {
-          double yq = __shfl_sync(0xffffffffu, acc, q) / L[(int64_t)(cb + q) * nb + cb + q];
-          if (lane == q) acc = yq;
-          else if (lane > q && lane < w) acc -= L[(int64_t)(cb + lane) * nb + cb + q] * yq;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if (q < w) {
+            const double dq = __shfl_sync(0xffffffffu, lr[q], q);
+            const double yq = __shfl_sync(0xffffffffu, acc, q) / dq;
+            if (lane == q) acc = yq;
+            else if (lane > q && lane < w) acc -= lr[q] * yq;
+          }
         }
         if (lane < w) ys[cb + lane] = acc;
       }
@@ -159,11 +167,20 @@ __global__ void __launch_bounds__(512) trsv_bwd_diag_kernel(Grid g, int i, doubl
         __syncthreads();
       }
       if (warp == 0) {
+        // stage column `lane` of the diagonal block (L[cb+q][cb+lane]) in registers
+        double lc[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          lc[q] = (lane < w && q < w) ? L[(int64_t)(cb + q) * nb + cb + lane] : 1.0;
         double acc = lane < w ? ys[cb + lane] : 0.0;
-        for (int q = w - 1; q >= 0; --q) {
-          double xq = __shfl_sync(0xffffffffu, acc, q) / L[(int64_t)(cb + q) * nb + cb + q];
-          if (lane == q) acc = xq;
-          else if (lane < q) acc -= L[(int64_t)(cb + q) * nb + cb + lane] * xq;
+#pragma unroll
+        for (int q = 31; q >= 0; --q) {
+          if (q < w) {
+            const double dq = __shfl_sync(0xffffffffu, lc[q], q);
+            const double xq = __shfl_sync(0xffffffffu, acc, q) / dq;
+            if (lane == q) acc = xq;
+            else if (lane < q) acc -= lc[q] * xq;
+          }
         }
         if (lane < w) ys[cb + lane] = acc;
       }

@@ -96,7 +96,10 @@ struct Work {
   int64_t slot0;
   int nitems;  // slots * nsub
   int nsubm, nsubn;
+  int* counter;  // dynamic work queue head (zeroed before the launch)
 };
+
+constexpr int SCHED = 4;  // work-item ring between the producer and the consumers
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc32_update_kernel(Grid g, int k, Work w, const __grid_constant__ CUtensorMap map_a,
@@ -110,7 +113,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + SCHED;
+  int* sitem = (int*)(sempty + SCHED);
+  uint32_t* tmem_slot = (uint32_t*)(sitem + SCHED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = g.nb;
@@ -125,6 +131,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
+    }
+    for (int s = 0; s < SCHED; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 5);  // MMA warp + 4 epilogue warps release a slot
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -146,12 +156,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     m0 = (sub / w.nsubn) * BM;
     n0 = (sub % w.nsubn) * BN;
   };
+  // consumers read the li-th work item from the ring (-1 = no more work)
+  auto next_item = [&](uint32_t li) {
+    const int s = li % SCHED;
+    mbar_wait(&sfull[s], (li / SCHED) & 1);
+    const int item = *(volatile int*)&sitem[s];
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&sempty[s]);
+    return item;
+  };
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+    // ------------------------------------------------ TMA producer + work queue
     if (lane == 0) {
       uint32_t it = 0;
-      for (int item = blockIdx.x; item < w.nitems; item += gridDim.x) {
+      for (uint32_t li = 0;; ++li) {
+        const int s = li % SCHED;
+        mbar_wait(&sempty[s], ((li / SCHED) & 1) ^ 1);
+        int item = atomicAdd(w.counter, 1);
+        if (item >= w.nitems) item = -1;
+        sitem[s] = item;
+        mbar_arrive(&sfull[s]);  // release: consumers see sitem[s]
+        if (item < 0) break;
         int i, j, m0, n0;
         item_ij(item, i, j, m0, n0);
         // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb
@@ -172,8 +198,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    uint32_t it = 0, li = 0;
-    for (int item = blockIdx.x; item < w.nitems; item += gridDim.x, ++li) {
+    uint32_t it = 0;
+    for (uint32_t li = 0;; ++li) {
+      if (next_item(li) < 0) break;
       const uint32_t b = li & 1, aph = (li >> 1) & 1;
       mbar_wait(&tempty[b], aph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -207,8 +234,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------ epilogue (warps 2..5)
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
-    uint32_t li = 0;
-    for (int item = blockIdx.x; item < w.nitems; item += gridDim.x, ++li) {
+    for (uint32_t li = 0;; ++li) {
+      const int item = next_item(li);
+      if (item < 0) break;
       int i, j, m0, n0;
       item_ij(item, i, j, m0, n0);
       const uint32_t b = li & 1, aph = (li >> 1) & 1;
@@ -314,11 +342,18 @@ int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, 
   w.nsubm = g.nb / BM;
   w.nsubn = g.nb / BN;
   w.nitems = (int)(scnt * w.nsubm * w.nsubn);
-  if (!g_sm_count) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_sm_count) cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+  // per-launch work-queue head: a rotating slot of a small per-device buffer
+  static int* counters[64] = {nullptr};
+  static unsigned next_counter[64] = {0};
+  if (dev < 0 || dev >= 64) { mt_set_error("device index out of range"); return MT_E_CUDA; }
+  if (!counters[dev] && mt_cuda_check(cudaMalloc(&counters[dev], 256 * sizeof(int)), "counter alloc"))
+    return MT_E_CUDA;
+  w.counter = counters[dev] + (next_counter[dev]++ % 256);
+  if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, sizeof(int), st), "counter reset"))
+    return MT_E_CUDA;
   int grid = ctas > 0 ? ctas : g_sm_count;
   if (grid > w.nitems) grid = w.nitems;
   const size_t smem = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;

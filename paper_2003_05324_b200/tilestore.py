@@ -10,6 +10,7 @@ for tests and inspection only -- the compute path never touches it.
 import ctypes
 import math
 import warnings
+import weakref
 from collections.abc import Mapping
 from dataclasses import dataclass
 from enum import Enum
@@ -99,7 +100,9 @@ class _TileView(Mapping):
     """Lazy {(i, j): Tile} view over the device pools (reference: the tiles dict)."""
 
     def __init__(self, owner):
-        self._m = owner
+        # weak: the matrix owns the view; a strong back-reference would form a
+        # cycle that keeps the (possibly 100+ GB) device pools alive after `del`
+        self._m = weakref.proxy(owner)
         self._cache = {}
 
     def _keys(self):
