@@ -69,6 +69,14 @@ typedef struct mt_tiles {
   float* split;  /* optional (MP, tensor-core engine): mt_split_tiles() FP32 tiles holding
                     the TF32 hi/lo split of the two panels in flight; NULL disables the
                     tcgen05 3xTF32 update (FFMA fallback kernel is used instead) */
+  /* multi-GPU (tile-column-cyclic 1 x g grid): this rank stores only tile
+   * columns j = col_offset + m * col_stride, in the same per-column pool order;
+   * col_stride = 1, col_offset = 0 is the single-GPU layout.  dpanel:
+   * mt_dpanel_tiles() FP64 tiles receiving the band rows of the panels in
+   * flight (NULL on a single GPU). */
+  int32_t col_stride;
+  int32_t col_offset;
+  double* dpanel;
 } mt_tiles;
 
 /* Matern parameters + per-theta Bessel constants (covmath.py:72-95, 228-283),
@@ -143,6 +151,28 @@ int mt_matvec_lower(const mt_tiles* g, const double* v, double* out, void* strea
 int mt_evaluate(const mt_tiles* g, const double* locs, int32_t metric, double radius,
                 const mt_matern* theta, const double* z, double* work, double* out2,
                 int32_t lookahead, void* stream);
+
+/* ---- multi-GPU factorization, one process per GPU (tile-column-cyclic layout,
+ * col_stride = #ranks, col_offset = rank).  The host drives the step loop and
+ * broadcasts each panel (split hi/lo rows k+1.. of panel k and the FP64 band
+ * rows in dpanel) from the column owner; every tile keeps the single-GPU
+ * update order, so the factor is bitwise identical for any rank count. */
+/* POTRF(k) + TRSM(k) of the owned tile column k (factor.py:249-265). */
+int mt_panel(const mt_tiles* g, int32_t k, void* stream);
+/* Step-k trailing updates of the owned columns in [jlo, jhi) (factor.py:266-274);
+ * panel k must be present in split/dpanel. */
+int mt_update(const mt_tiles* g, int32_t k, int32_t jlo, int32_t jhi, void* stream);
+/* partial[k] = sum log diag(L_kk) for owned k, 0 otherwise (factor.py:318-323). */
+int mt_logdet_partials(const mt_tiles* g, double* partial, void* stream);
+/* Forward-sweep step i on the owner of column i: y_i = L_ii^{-1} x_i, x_r -= L_ri y_i. */
+int mt_fwd_step(const mt_tiles* g, int32_t i, double* x, void* stream);
+/* Sum of squares of m device doubles with mt_quad's fixed-order reduction
+ * (work: >= 1024 device doubles) -> *out (device). */
+int mt_sumsq(const double* x, int64_t m, double* work, double* out, void* stream);
+/* Local pool sizes (tiles) of a rank's columns; dpanel ring size. */
+int mt_local_tiles(int32_t p, int32_t t, int32_t mode, int32_t col_stride, int32_t col_offset,
+                   int64_t* ndp, int64_t* nsp);
+int64_t mt_dpanel_tiles(int32_t p, int32_t t, int32_t mode);
 
 /* Synchronise `stream` and read status: *bad_pivot (-1 none), *overflow,
  * *duplicates.  Returns MT_E_NOT_SPD / MT_E_OVERFLOW when set, else MT_OK. */

@@ -30,6 +30,9 @@ class MtTiles(ctypes.Structure):
         ("scratch", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
         ("split", ctypes.c_void_p),
+        ("col_stride", ctypes.c_int32),
+        ("col_offset", ctypes.c_int32),
+        ("dpanel", ctypes.c_void_p),
     ]
 
 
@@ -80,6 +83,13 @@ SIGNATURES = {
     "mt_get_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
     "mt_put_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
     "mt_set_option": (_I32, [_I32, _I32]),
+    "mt_panel": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
+    "mt_update": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V]),
+    "mt_logdet_partials": (ctypes.c_int, [_P(MtTiles), _V, _V]),
+    "mt_fwd_step": (ctypes.c_int, [_P(MtTiles), _I32, _V, _V]),
+    "mt_sumsq": (ctypes.c_int, [_V, _I64, _V, _V, _V]),
+    "mt_local_tiles": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _P(_I64), _P(_I64)]),
+    "mt_dpanel_tiles": (_I64, [_I32, _I32, _I32]),
     "mt_launch_count": (ctypes.c_longlong, []),
     "mt_prof_begin": (ctypes.c_int, [_I32]),
     "mt_prof_end": (ctypes.c_int, [_I32, _V, _V, _V, _V]),

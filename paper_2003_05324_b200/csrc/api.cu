@@ -32,6 +32,9 @@ int mt_logdet_impl(const Grid& g, double* out, double* work, cudaStream_t st);
 int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_t st);
 int mt_quad_impl(const Grid& g, const double* z, double* work, double* out, cudaStream_t st);
 int mt_matvec_lower_impl(const Grid& g, const double* v, double* out, cudaStream_t st);
+int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st);
+int mt_logdet_partials_impl(const Grid& g, double* partial, cudaStream_t st);
+int mt_sumsq_impl(const double* x, int64_t m, double* work, double* out, cudaStream_t st);
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[512] = "";
@@ -58,8 +61,17 @@ static int check_layout(const mt_tiles* g) {
   if (!g || g->n < 1 || g->nb < 1 || g->p != (int32_t)((g->n + g->nb - 1) / g->nb) ||
       g->t < 1 || g->t > g->p || g->mode < 0 || g->mode > 2 ||
       (g->mode == MT_MODE_DP && g->t != g->p) || !g->dp_pool || !g->status ||
-      !g->scratch || (g->mode == MT_MODE_MP && g->t < g->p && !g->sp_pool)) {
+      !g->scratch || (g->mode == MT_MODE_MP && g->t < g->p && !g->sp_pool) ||
+      g->col_stride < 0 || (g->col_stride > 1 && (g->col_offset < 0 ||
+                                                  g->col_offset >= g->col_stride || !g->dpanel))) {
     mt_set_error("bad tile layout descriptor");
+    return MT_E_BAD_ARG;
+  }
+  return MT_OK;
+}
+static int single_gpu_only(const mt_tiles* g, const char* what) {
+  if (g->col_stride > 1) {
+    mt_set_error("%s operates on the full matrix; use the per-step multi-GPU entry points", what);
     return MT_E_BAD_ARG;
   }
   return MT_OK;
@@ -269,7 +281,61 @@ int mt_matern_array(const double* r, int64_t m, const mt_matern* theta, double* 
 
 int mt_cholesky(const mt_tiles* t, int32_t lookahead, void* stream) {
   RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_cholesky"));
   return cholesky_schedule(make_grid(t), lookahead, (cudaStream_t)stream);
+}
+
+// ---- per-step entry points of the multi-GPU (tile-column-cyclic) factorization
+int mt_panel(const mt_tiles* t, int32_t k, void* stream) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  if (k < 0 || k >= g.p || !g.owns_col(k)) {
+    mt_set_error("mt_panel: rank does not own tile column %d", k);
+    return MT_E_BAD_ARG;
+  }
+  const int narrow = (g.mode == MT_MODE_MP && k + g.t <= g.p - 1) ? 1 : 0;
+  RC(mt_potrf_impl(g, k, narrow, (cudaStream_t)stream));
+  if (k + 1 < g.p) RC(mt_trsm_impl(g, k, (cudaStream_t)stream));
+  return MT_OK;
+}
+
+int mt_update(const mt_tiles* t, int32_t k, int32_t jlo, int32_t jhi, void* stream) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  if (k < 0 || k >= g.p || jlo <= k || jhi > g.p) {
+    mt_set_error("mt_update: bad step/column range");
+    return MT_E_BAD_ARG;
+  }
+  return mt_update_impl(g, k, jlo, jhi, (cudaStream_t)stream);
+}
+
+int mt_logdet_partials(const mt_tiles* t, double* partial, void* stream) {
+  RC(check_layout(t));
+  return mt_logdet_partials_impl(make_grid(t), partial, (cudaStream_t)stream);
+}
+
+int mt_fwd_step(const mt_tiles* t, int32_t i, double* x, void* stream) {
+  RC(check_layout(t));
+  return mt_fwd_step_impl(make_grid(t), i, x, (cudaStream_t)stream);
+}
+
+int mt_sumsq(const double* x, int64_t m, double* work, double* out, void* stream) {
+  if (!x || !work || !out || m < 0) { mt_set_error("mt_sumsq: bad arguments"); return MT_E_BAD_ARG; }
+  return mt_sumsq_impl(x, m, work, out, (cudaStream_t)stream);
+}
+
+int mt_local_tiles(int32_t p, int32_t t_, int32_t mode, int32_t col_stride, int32_t col_offset,
+                   int64_t* ndp, int64_t* nsp) {
+  Grid g{};
+  g.p = p; g.t = mode == MT_MODE_DP ? p : t_; g.mode = mode;
+  g.cs = col_stride > 0 ? col_stride : 1; g.c0 = col_offset;
+  if (ndp) *ndp = g.nband();
+  if (nsp) *nsp = g.noff();
+  return MT_OK;
+}
+
+int64_t mt_dpanel_tiles(int32_t p, int32_t t_, int32_t mode) {
+  return 2 * (int64_t)(mode == MT_MODE_DP ? p : t_);
 }
 
 int64_t mt_work_doubles(const mt_tiles* t) {
@@ -278,22 +344,26 @@ int64_t mt_work_doubles(const mt_tiles* t) {
 
 int mt_logdet(const mt_tiles* t, double* work, double* out, void* stream) {
   RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_logdet"));
   return mt_logdet_impl(make_grid(t), out, work, (cudaStream_t)stream);
 }
 
 int mt_solve(const mt_tiles* t, double* x, int64_t nrhs, int32_t which, void* stream) {
   RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_solve"));
   if (nrhs < 1 || which < 1 || which > 3) { mt_set_error("bad solve arguments"); return MT_E_BAD_ARG; }
   return mt_solve_impl(make_grid(t), x, nrhs, which, (cudaStream_t)stream);
 }
 
 int mt_quad(const mt_tiles* t, const double* z, double* work, double* out, void* stream) {
   RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_quad"));
   return mt_quad_impl(make_grid(t), z, work, out, (cudaStream_t)stream);
 }
 
 int mt_matvec_lower(const mt_tiles* t, const double* v, double* out, void* stream) {
   RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_matvec_lower"));
   return mt_matvec_lower_impl(make_grid(t), v, out, (cudaStream_t)stream);
 }
 
@@ -311,6 +381,7 @@ int mt_evaluate(const mt_tiles* t, const double* locs, int32_t metric, double ra
                 const mt_matern* theta, const double* z, double* work, double* out2,
                 int32_t lookahead, void* stream) {
   RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_evaluate"));
   const Grid g = make_grid(t);
   cudaStream_t st = (cudaStream_t)stream;
   RC(mt_generate_impl(g, locs, metric, radius, *theta, st));
@@ -341,7 +412,8 @@ static int tile_xfer(const mt_tiles* t, int32_t i, int32_t j, int32_t which, voi
                      cudaStream_t st) {
   RC(check_layout(t));
   const Grid g = make_grid(t);
-  if (i < 0 || j < 0 || i >= g.p || j > i || !g.present(i, j) || (which == 0) != g.band(i, j)) {
+  if (i < 0 || j < 0 || i >= g.p || j > i || !g.present(i, j) || (which == 0) != g.band(i, j) ||
+      !g.owns_col(j)) {
     mt_set_error("tile (%d,%d) not stored in the requested pool", i, j);
     return MT_E_BAD_ARG;
   }

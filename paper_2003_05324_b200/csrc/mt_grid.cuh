@@ -24,6 +24,10 @@ struct Grid {
   float* scratch;
   int64_t* status;
   float* split;
+  // multi-GPU tile-column-cyclic ownership: this rank stores tile columns
+  // j = c0, c0 + cs, c0 + 2cs, ... (single GPU: cs = 1, c0 = 0)
+  int cs = 1, c0 = 0;
+  double* dpanel = nullptr;  // multi-GPU: FP64 band rows of the panels in flight
 
   MT_HD int64_t tile_elems() const { return (int64_t)nb * nb; }
   MT_HD bool band(int i, int j) const { return (i - j) < t; }
@@ -33,23 +37,34 @@ struct Grid {
     int64_t r = n - (int64_t)i * nb;
     return r < nb ? (int)r : nb;
   }
+  MT_HD bool owns_col(int j) const { return j >= c0 && (j - c0) % cs == 0; }
+  // number of owned tile columns j' < j
+  MT_HD int owned_before(int j) const { return j <= c0 ? 0 : (j - c0 + cs - 1) / cs; }
+  MT_HD int owned_cols() const { return owned_before(p); }
+  MT_HD int owned_col(int m) const { return c0 + m * cs; }
 
-  // first band-pool slot of tile column j: sum_{j'<j} min(t, p - j')
+  // first band-pool slot of tile column j: sum over owned j' < j of min(t, p - j')
   MT_HD int64_t bcol(int j) const {
-    int64_t q = p - t;
-    if (j <= q) return (int64_t)j * t;
-    int64_t a = p - j;
-    return q * t + ((int64_t)t * (t + 1) - a * (a + 1)) / 2;
+    const int m = owned_before(j);
+    const int m1 = owned_before(p - t + 1);  // owned columns holding t band tiles
+    if (m <= m1) return (int64_t)m * t;
+    return (int64_t)m1 * t + (int64_t)(m - m1) * (p - c0) -
+           (int64_t)cs * ((int64_t)m * (m - 1) / 2 - (int64_t)m1 * (m1 - 1) / 2);
   }
-  // first off-band-pool slot of tile column j: sum_{j'<j} max(0, p - t - j')
+  // first off-band-pool slot of tile column j: sum over owned j' < j of max(0, p - t - j')
   MT_HD int64_t scol(int j) const {
-    int64_t q = p - t;
+    const int64_t q = p - t;
     if (q <= 0) return 0;
-    if (j >= q) return q * (q + 1) / 2;
-    return (int64_t)j * q - (int64_t)j * (j - 1) / 2;
+    const int ma = owned_before(j), mb = owned_before((int)q);
+    const int mm = ma < mb ? ma : mb;
+    return (int64_t)mm * (q - c0) - (int64_t)cs * ((int64_t)mm * (mm - 1) / 2);
   }
   MT_HD int64_t nband() const { return bcol(p); }
   MT_HD int64_t noff() const { return mode == MT_MODE_MP ? scol(p) : 0; }
+  // multi-GPU panel ring: FP64 copy of band rows i in [k, k + t) of panel k
+  MT_HD double* dpanel_tile(int i, int k) const {
+    return dpanel + ((int64_t)(k & 1) * t + (i - k)) * tile_elems();
+  }
 
   MT_HD double* dtile(int i, int j) const { return dp + (bcol(j) + (i - j)) * tile_elems(); }
   MT_HD float* stile(int i, int j) const { return sp + (scol(j) + (i - j - t)) * tile_elems(); }
@@ -82,24 +97,24 @@ struct Grid {
     return band(i, k) ? smirror(i, k) : stile(i, k);
   }
 
-  // slot -> (i, j) inversion by binary search over the column starts
+  // slot -> (i, j) inversion by binary search over the owned column starts
   __device__ __forceinline__ void band_slot_ij(int64_t s, int& i, int& j) const {
-    int lo = 0, hi = p;  // find largest j with bcol(j) <= s
+    int lo = 0, hi = owned_cols();  // largest owned index m with bcol(col m) <= s
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
-      if (bcol(mid) <= s) lo = mid; else hi = mid;
+      if (bcol(owned_col(mid)) <= s) lo = mid; else hi = mid;
     }
-    j = lo;
-    i = lo + (int)(s - bcol(lo));
+    j = owned_col(lo);
+    i = j + (int)(s - bcol(j));
   }
   __device__ __forceinline__ void off_slot_ij(int64_t s, int& i, int& j) const {
-    int lo = 0, hi = p - t;
+    int lo = 0, hi = owned_before(p - t);
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
-      if (scol(mid) <= s) lo = mid; else hi = mid;
+      if (scol(owned_col(mid)) <= s) lo = mid; else hi = mid;
     }
-    j = lo;
-    i = lo + t + (int)(s - scol(lo));
+    j = owned_col(lo);
+    i = j + t + (int)(s - scol(j));
   }
   __device__ __forceinline__ bool failed() const {
     return *(volatile int64_t*)status >= 0;
@@ -111,6 +126,9 @@ inline Grid make_grid(const mt_tiles* g) {
   r.n = g->n; r.nb = g->nb; r.p = g->p; r.t = g->t; r.mode = g->mode;
   r.dp = g->dp_pool; r.sp = g->sp_pool; r.scratch = g->scratch; r.status = g->status;
   r.split = g->split;
+  r.cs = g->col_stride > 0 ? g->col_stride : 1;
+  r.c0 = g->col_offset;
+  r.dpanel = g->dpanel;
   return r;
 }
 

@@ -38,6 +38,10 @@ __device__ __forceinline__ bool tile_ref(const Grid& g, int i, int j, TileRef& t
 // ------------------------------------------------------------------ logdet
 __global__ void __launch_bounds__(256) logdet_partial_kernel(Grid g, double* partial) {
   const int k = blockIdx.x;
+  if (!g.owns_col(k)) {  // multi-GPU: another rank holds this diagonal tile
+    if (threadIdx.x == 0) partial[k] = 0.0;
+    return;
+  }
   const double* L = g.dtile(k, k);
   const int nb = g.nb;
   double s = 0.0;
@@ -305,6 +309,45 @@ int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_
       }
     }
   }
+  return MT_OK;
+}
+
+// multi-GPU forward sweep, step i (on the owner of tile column i): y_i = L_ii^{-1} x_i,
+// then x_r -= L_ri y_i for r > i -- the same launches and order as mt_solve_impl
+int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st) {
+  const int nb = g.nb, p = g.p;
+  if (!g.owns_col(i)) { mt_set_error("rank does not own tile column %d", i); return MT_E_BAD_ARG; }
+  const size_t smem = (size_t)nb * sizeof(double);
+  cudaFuncSetAttribute(trsv_fwd_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(smem > 48 * 1024 ? smem : 48 * 1024));
+  ProfScope ps(MT_K_SOLVE, st, 2.0 * (double)nb * nb * (p - i), (double)nb * nb * 8.0 * (p - i), 2);
+  trsv_fwd_diag_kernel<<<1, 512, smem, st>>>(g, i, x, 1);
+  MT_LAUNCH_CHECK("trsv_fwd_diag");
+  if (i + 1 < p) {
+    const int nrb = (nb + kGemvRows - 1) / kGemvRows;
+    gemv_fwd_kernel<<<(unsigned)((p - i - 1) * nrb), 256, 0, st>>>(g, i, x, 1, nrb);
+    MT_LAUNCH_CHECK("gemv_fwd");
+  }
+  return MT_OK;
+}
+
+// per-diagonal-tile log-sums (0 for tiles another rank owns); fixed-order sum elsewhere
+int mt_logdet_partials_impl(const Grid& g, double* partial, cudaStream_t st) {
+  ProfScope ps(MT_K_MISC, st, 0.0, (double)g.p * g.nb * 8.0);
+  logdet_partial_kernel<<<g.p, 256, 0, st>>>(g, partial);
+  MT_LAUNCH_CHECK("logdet_partial");
+  return MT_OK;
+}
+
+// sum of squares of m doubles with the fixed-order reduction used by mt_quad
+// (work: >= 1024 doubles)
+int mt_sumsq_impl(const double* x, int64_t m, double* work, double* out, cudaStream_t st) {
+  const int blocks = 1024;
+  ProfScope ps(MT_K_MISC, st, 2.0 * m, m * 8.0, 2);
+  sumsq_partial_kernel<<<blocks, 256, 0, st>>>(x, m, work);
+  MT_LAUNCH_CHECK("sumsq_partial");
+  fixed_sum_kernel<<<1, 1, 0, st>>>(work, blocks, 1.0, out);
+  MT_LAUNCH_CHECK("fixed_sum");
   return MT_OK;
 }
 

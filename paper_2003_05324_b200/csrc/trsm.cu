@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool fp32_operand = (sizeof(T) == 4) || (M != nullptr);
   float* SH = (g.split && fp32_operand) ? g.split_hi(i, k) : nullptr;
   float* SL = SH ? g.split_lo(i, k) : nullptr;
+  double* DP = (sizeof(T) == 8 && g.cs > 1 && g.dpanel) ? g.dpanel_tile(i, k) : nullptr;
   for (int r = threadIdx.x >> 5; r < nr; r += kThreads / 32) {
     for (int cc = c; cc < nb; cc += 32) {
       const T v = Xt[(size_t)cc * XS + r];
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       B[o] = v;
       const float f = __double2float_rn((double)v);
       if (M) M[o] = f;
+      if (DP) DP[o] = (double)v;  // multi-GPU: FP64 band panel row for the broadcast
       if (SH) {
         uint32_t h;
         asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));

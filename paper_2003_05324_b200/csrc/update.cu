@@ -191,24 +191,59 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// 8 consecutive operand values (FP64, or FP32 widened) starting at idx
-__device__ __forceinline__ void ld8(const void* base, bool f32, int64_t idx, double (&v)[8]) {
-  if (f32) {
-    const float4* p = (const float4*)((const float*)base + idx);
+// FP64 view of an operand tile of panel k: FP64 payload, FP32 payload (widened),
+// or -- on a multi-GPU rank that received the panel -- the TF32 split hi + lo,
+// whose FP64 sum is exactly the FP32 payload (lo = x - hi is exact in FP32)
+struct Operand {
+  const void* base;
+  const float* lo;  // non-null: hi/lo split
+  bool f32;
+};
+__device__ __forceinline__ Operand panel_operand(const Grid& g, int i, int k) {
+  Operand o;
+  o.lo = nullptr;
+  if (g.band(i, k)) {
+    o.base = g.cs == 1 ? (const void*)g.dtile(i, k) : (const void*)g.dpanel_tile(i, k);
+    o.f32 = false;
+  } else if (g.cs == 1) {
+    o.base = g.stile(i, k);
+    o.f32 = true;
+  } else {
+    o.base = g.split_hi(i, k);
+    o.lo = g.split_lo(i, k);
+    o.f32 = true;
+  }
+  return o;
+}
+
+// 8 consecutive operand values starting at idx, as FP64
+__device__ __forceinline__ void ld8(const Operand& o, int64_t idx, double (&v)[8]) {
+  if (o.f32) {
+    const float4* p = (const float4*)((const float*)o.base + idx);
     float4 x = p[0], y = p[1];
     v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+    if (o.lo) {
+      const float4* q = (const float4*)(o.lo + idx);
+      float4 a = q[0], b = q[1];
+      v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+      v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+    }
   } else {
-    const double2* p = (const double2*)((const double*)base + idx);
+    const double2* p = (const double2*)((const double*)o.base + idx);
 #pragma unroll
     for (int q = 0; q < 4; ++q) { double2 t = p[q]; v[2 * q] = t.x; v[2 * q + 1] = t.y; }
   }
 }
-__device__ __forceinline__ void ld4(const void* base, bool f32, int64_t idx, double (&v)[4]) {
-  if (f32) {
-    float4 x = *(const float4*)((const float*)base + idx);
+__device__ __forceinline__ void ld4(const Operand& o, int64_t idx, double (&v)[4]) {
+  if (o.f32) {
+    float4 x = *(const float4*)((const float*)o.base + idx);
     v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    if (o.lo) {
+      float4 a = *(const float4*)(o.lo + idx);
+      v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w;
+    }
   } else {
-    const double2* p = (const double2*)((const double*)base + idx);
+    const double2* p = (const double2*)((const double*)o.base + idx);
     double2 s = p[0], t = p[1];
     v[0] = s.x; v[1] = s.y; v[2] = t.x; v[3] = t.y;
   }
@@ -227,9 +262,7 @@ __global__ void __launch_bounds__(256, 2)
   const bool syrk = (i == j);
   if (syrk && n0 >= m0 + MBM) return;  // entirely above the diagonal
   const int nb = g.nb;
-  const bool fa = !g.band(i, k), fb = !g.band(j, k);
-  const void* A = fa ? (const void*)g.stile(i, k) : (const void*)g.dtile(i, k);
-  const void* B = fb ? (const void*)g.stile(j, k) : (const void*)g.dtile(j, k);
+  const Operand A = panel_operand(g, i, k), B = panel_operand(g, j, k);
   double* __restrict__ C = g.dtile(i, j);
 
   extern __shared__ __align__(16) double msm[];
@@ -248,8 +281,8 @@ __global__ void __launch_bounds__(256, 2)
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   double ra[8], rb[4];
-  ld8(A, fa, abase, ra);
-  ld4(B, fb, bbase, rb);
+  ld8(A, abase, ra);
+  ld4(B, bbase, rb);
   int buf = 0;
   for (int kk = 0; kk < nb; kk += MBK) {
     double* as = As + buf * MBM * MLD;
@@ -260,8 +293,8 @@ __global__ void __launch_bounds__(256, 2)
     *(double2*)&bs[br * MLD + bc + 2] = make_double2(rb[2], rb[3]);
     __syncthreads();
     if (kk + MBK < nb) {
-      ld8(A, fa, abase + kk + MBK, ra);
-      ld4(B, fb, bbase + kk + MBK, rb);
+      ld8(A, abase + kk + MBK, ra);
+      ld4(B, bbase + kk + MBK, rb);
     }
 #pragma unroll
     for (int k4 = 0; k4 < MBK; k4 += 4) {
@@ -341,6 +374,7 @@ static void update_flops(const Grid& g, int k, int jlo, int jhi, double& f64, do
   f64 = f32 = 0.0;
   const double rk = g.rows(k);
   for (int j = jlo; j < jhi; ++j) {
+    if (!g.owns_col(j)) continue;
     const double rj = g.rows(j);
     const int iband = j + g.t < g.p ? j + g.t : g.p;  // band rows [j, iband)
     for (int i = j; i < iband; ++i) {
@@ -358,6 +392,10 @@ static void update_flops(const Grid& g, int k, int jlo, int jhi, double& f64, do
 int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   if (jlo >= jhi) return MT_OK;
   const int nb = g.nb;
+  if (g.cs > 1 && (nb % MBM != 0 || (g.mode == MT_MODE_MP && !mt_tc_supported(g)))) {
+    mt_set_error("multi-GPU layout needs nb %% 256 == 0 and the tcgen05 engine (split buffer)");
+    return MT_E_BAD_ARG;
+  }
   double f64, f32;
   update_flops(g, k, jlo, jhi, f64, f32);
   // band (FP64) outputs in columns [jlo, jhi)
@@ -382,7 +420,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
   if (scnt > 0) {
     ProfScope ps(MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
-    if (mt_opt_engine() == MT_ENGINE_TF32X3 && mt_tc_supported(g)) {
+    if ((mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) && mt_tc_supported(g)) {
       // the panel-column update (jhi == jlo + 1) runs beside the bulk update:
       // keep it narrow; the bulk update may be capped to leave SMs for the panel
       const int ctas = (jhi == jlo + 1) ? 16 : mt_opt_update_ctas();

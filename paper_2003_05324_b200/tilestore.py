@@ -107,7 +107,7 @@ class _TileView(Mapping):
 
     def _keys(self):
         m = self._m
-        for j in range(m.p):
+        for j in range(m.col_offset, m.p, m.col_stride):  # owned tile columns
             for i in range(j, m.p):
                 if m.policy.mode.value != "dst" or i - j < m.policy.diag_thick:
                     yield (i, j)
@@ -124,7 +124,8 @@ class _TileView(Mapping):
         except (TypeError, ValueError):
             return False
         m = self._m
-        return (0 <= j <= i < m.p
+        return (0 <= j <= i < m.p and (j - m.col_offset) % m.col_stride == 0
+                and j >= m.col_offset
                 and (m.policy.mode.value != "dst" or i - j < m.policy.diag_thick))
 
     def __getitem__(self, key):
@@ -145,7 +146,7 @@ class TileMatrix:
     here (use `from_dense` to upload explicit payloads).
     """
 
-    def __init__(self, n, nb, policy, device=None):
+    def __init__(self, n, nb, policy, device=None, col_stride=1, col_offset=0):
         if n < 1:
             raise ValueError(f"need n >= 1, got {n}")
         if nb < 1:
@@ -158,24 +159,34 @@ class TileMatrix:
         self.duplicate_locations = False
         self.factored = False
         self._version = 0
+        # multi-GPU: this rank stores tile columns col_offset + m * col_stride only
+        self.col_stride, self.col_offset = int(col_stride), int(col_offset)
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         lib = _lib.load()
         mode = _lib.MODE_CODE[self.policy.mode.value]
         t = self.policy.diag_thick
         te = self.nb * self.nb
-        ndp = lib.mt_dp_tiles(self.p, t, mode)
-        nsp = lib.mt_sp_tiles(self.p, t, mode)
+        ndp, nsp = ctypes.c_int64(), ctypes.c_int64()
+        lib.mt_local_tiles(self.p, t, mode, self.col_stride, self.col_offset,
+                           ctypes.byref(ndp), ctypes.byref(nsp))
+        ndp, nsp = ndp.value, nsp.value
         nsc = lib.mt_scratch_tiles(self.p, t, mode, self.nb)
         nsl = lib.mt_split_tiles(self.p, t, mode) if self.nb % 256 == 0 else 0
         self.dp_pool = torch.empty(max(ndp, 1) * te, dtype=torch.float64, device=dev)
         self.sp_pool = torch.empty(max(nsp, 1) * te, dtype=torch.float32, device=dev)
         self.scratch = torch.empty(max(nsc, 1) * te, dtype=torch.float32, device=dev)
         self.split = (torch.empty(nsl * te, dtype=torch.float32, device=dev) if nsl else None)
+        self.dpanel = None
+        if self.col_stride > 1:
+            self.dpanel = torch.empty(lib.mt_dpanel_tiles(self.p, t, mode) * te,
+                                      dtype=torch.float64, device=dev)
         self.status = torch.empty(4, dtype=torch.int64, device=dev)
         self.desc = _lib.MtTiles(self.n, self.nb, self.p, t, mode, self.dp_pool.data_ptr(),
                                  self.sp_pool.data_ptr(), self.scratch.data_ptr(),
                                  self.status.data_ptr(),
-                                 self.split.data_ptr() if self.split is not None else 0)
+                                 self.split.data_ptr() if self.split is not None else 0,
+                                 self.col_stride, self.col_offset,
+                                 self.dpanel.data_ptr() if self.dpanel is not None else 0)
         self.reset_status()
         self.tiles = _TileView(self)
 
