@@ -3,29 +3,36 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one full log-likelihood evaluation of BASELINE.json configs[1]
-(N = 65,536 locations, tile 512, MP band t = 2, Matern (1, 0.1, 0.5)):
-covariance generation -> band-precision tile Cholesky -> logdet -> quadratic
-form, all on the device.  Prints ONE JSON line (rank 0).
+Workload (BASELINE.json metric, "at N=262144"): one step = one full
+log-likelihood evaluation at N = 262,144 locations, tile 512, MP band t = 8,
+Matern (1, 0.1, 0.5) on a Morton-sorted synthetic field -- covariance
+generation -> band-precision tile Cholesky -> logdet -> quadratic form, all on
+the device.  MP at this size needs 142 GB, so it fits one B200; with N > 1 the
+same evaluation is split over the ranks (tile-column-cyclic layout, NCCL panel
+broadcasts; strong scaling).  Prints ONE JSON line (rank 0).
 
   value      whole-job loglik evaluations/s, inputs resident in HBM, device time
-             (CUDA events, max over ranks).  Also cholesky_tflops = (N^3/3)/T_chol.
-  e2e        the same metric through the public API `loglik(dataset, ...)` from
-             host numpy buffers (pinned H2D of locations + z, D2H of the result).
-  roofline   dominant kernel's achieved TFLOP/s from CUDA events recorded around
-             every launch inside the timed region vs a measured FMA peak.
+             (CUDA events on the launching stream, max over ranks).
+             cholesky_tflops = (N^3/3) / T_chol, T_chol timed inside each step.
+  e2e        the same metric through the public API `loglik(dataset, ...)`
+             (`loglik_distributed` for N > 1) from pinned host buffers: H2D of
+             locations + z and D2H of the result inside the timed region.
+  roofline   dominant kernel (the tcgen05 3xTF32 bulk update): algorithmic
+             flops per launch / average launch duration from CUDA events
+             recorded around every launch inside the timed region; plus the
+             flop-weighted FP64/FP32 roofline of the whole factorization.
+  mp_vs_dp   the build's own full-DP path timed the same way (at N = 262144
+             when it fits the ranks' memory, else at configs[1] N = 65536).
   cpu_baseline  the reference algorithm (oracle port: same LAPACK/BLAS calls as
              the reference) on the host cores, bounded sample, extrapolated.
-  mp_vs_dp   the build's own full-DP evaluation timed the same way.
 
-With --gpus N > 1 (torchrun, one rank per GPU) every rank evaluates its own
-likelihood replica (weak scaling; the 2D block-cyclic distributed factor is
-not in this round).  --impl reference times only the CPU reference arm.
+--impl reference times only the CPU reference arm (rank 0).
 """
 
 import argparse
+import ctypes
+import gc
 import json
-import math
 import os
 import subprocess
 import sys
@@ -38,19 +45,24 @@ sys.path.insert(0, ROOT)
 METRIC = ("Mixed-precision Cholesky TFLOP/s + loglik evals/s at N=262144, 1-8 B200 vs full-DP")
 UNIT = "loglik evals/s"
 THETA = (1.0, 0.1, 0.5)
-KINDS = ["gen64", "gen32", "potrf", "trsm64", "trsm32", "upd64", "upd32", "solve", "misc"]
+KINDS = ["gen64", "gen32", "potrf", "trsm64", "trsm32", "upd64", "upd32", "solve", "misc",
+         "upd64p", "upd32p"]
+# profiling recipe fallback (B200_PROFILING.md) when MEASURED_PEAKS.json is absent
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--n", type=int, default=262144)
     ap.add_argument("--nb", type=int, default=512)
-    ap.add_argument("--t", type=int, default=2)
-    ap.add_argument("--dp-steps", type=int, default=1)
+    ap.add_argument("--t", type=int, default=8)
+    ap.add_argument("--dp-n", type=int, default=65536,
+                    help="N of the MP-vs-DP comparison when full DP at --n does not fit")
+    ap.add_argument("--dp-t", type=int, default=2)
     ap.add_argument("--cpu-n", type=int, default=16384, help="CPU baseline sample size")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dp", action="store_true")
@@ -105,6 +117,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "MEASURED_PEAKS.json (of measured)"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "B200_PROFILING.md fallback (of fallback; MEASURED_PEAKS.json absent)"
+
+
 # --------------------------------------------------------------- CPU baseline
 def cpu_reference_sample(n, nb, t, reps=1):
     """Time the reference algorithm (oracle port) for one MP evaluation at n on
@@ -118,6 +138,7 @@ def cpu_reference_sample(n, nb, t, reps=1):
     cores = os.cpu_count() or 1
     locs = generate_locations(n, seed=derive_seed(0, 0))
     ds, _ = morton_sort(GeoDataset(locs, np.random.default_rng(7).standard_normal(n)))
+    t = min(t, -(-n // nb))
     best = best_chol = float("inf")
     with threadpool_limits(limits=cores):
         for _ in range(reps):
@@ -142,7 +163,7 @@ def cpu_reference_sample(n, nb, t, reps=1):
 
 
 def cpu_baseline_obj(args):
-    sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t)
+    sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t, reps=2)
     scale = (args.cpu_n / args.n) ** 3
     return {
         "value": (1.0 / sec) * scale,
@@ -150,8 +171,8 @@ def cpu_baseline_obj(args):
         "cores": cores,
         "kind": "port",
         "sample": (f"oracle port of the reference (same dpotrf/dtrsm/strsm/dsyrk/dgemm/sgemm "
-                   f"calls) for one MP t={args.t} nb={args.nb} evaluation at N={args.cpu_n}: "
-                   f"{sec:.2f} s ({chol:.2f} s Cholesky = "
+                   f"calls), best of 2 MP t={min(args.t, args.cpu_n // args.nb)} nb={args.nb} "
+                   f"evaluations at N={args.cpu_n}: {sec:.2f} s ({chol:.2f} s Cholesky = "
                    f"{args.cpu_n ** 3 / 3 / chol / 1e9:.1f} GFLOP/s); value extrapolated to "
                    f"N={args.n} by the N^3 flop count"),
         "cpu_cholesky_gflops": args.cpu_n ** 3 / 3 / chol / 1e9,
@@ -165,6 +186,7 @@ def run_reference(args, rank):
     for _ in range(max(0, args.warmup)):
         cpu_reference_sample(args.cpu_n, args.nb, args.t)
     times = []
+    cores, info = 1, {}
     for _ in range(max(1, args.steps)):
         sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t)
         times.append(sec)
@@ -173,20 +195,34 @@ def run_reference(args, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-        "config": {"workload": f"configs[1] sample: MP t={args.t} nb={args.nb} N={args.cpu_n} "
-                               f"extrapolated to N={args.n}", "n": args.n, "nb": args.nb,
-                   "band_t": args.t},
+        "config": {"workload": f"MP t={args.t} nb={args.nb} loglik at N={args.n}: sampled at "
+                               f"N={args.cpu_n} on the host CPU, extrapolated by N^3",
+                   "n": args.n, "nb": args.nb, "band_t": args.t},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"one MP evaluation at N={args.cpu_n} per step, "
-                                   f"extrapolated by N^3", **info},
+                         "sample": f"one MP evaluation at N={args.cpu_n} per step "
+                                   f"(oracle port, all host threads), extrapolated by N^3", **info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------- GPU arm
+def _dataset(mt, n, seed_rank=0):
+    import numpy as np
+    locs = mt.generate_locations(n, seed=mt.derive_seed(seed_rank, 0))
+    z = np.random.default_rng(mt.derive_seed(seed_rank, 1)).standard_normal(n)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, z))
+    return ds
+
+
+def _free_memory():
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -194,223 +230,218 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2003_05324_b200 as mt
     from paper_2003_05324_b200 import _lib
+    from paper_2003_05324_b200.distributed import DistributedEvaluator, loglik_distributed
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     lib = _lib.load()
+    dist_on = world > 1
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
+        if not dist_on:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def make_eval(asm, pol):
+        return DistributedEvaluator(asm, pol) if dist_on else mt.Evaluator(asm, pol)
+
+    def run_eval(ev, th, chol_events=None):
+        if dist_on:
+            return ev(th, chol_events=chol_events)
+        ev.launch(th, chol_events=chol_events)
+        return ev.finish()
+
     n, nb, t = args.n, args.nb, args.t
-    locs = mt.generate_locations(n, seed=mt.derive_seed(rank, 0))
-    z = np.random.default_rng(mt.derive_seed(rank, 1)).standard_normal(n)
-    ds, _ = mt.morton_sort(mt.GeoDataset(locs, z))
+    ds = _dataset(mt, n)  # same dataset on every rank (one distributed evaluation)
     theta = mt.MaternParams(*THETA)
     mp_pol = mt.PrecisionPolicy.mp(diag_thick=t)
-
     asm = mt.TileAssembler(ds, nb)
-    ev = mt.Evaluator(asm, mp_pol)
-    for _ in range(max(3, args.warmup)):
-        ev(theta)
+    ev = make_eval(asm, mp_pol)
+    warm = max(3, args.warmup)
+    for _ in range(warm):
+        run_eval(ev, theta)
 
     # ---- timed region: K evaluations, inputs resident in HBM
     clocks = ClockSampler(local_rank)
     st = torch.cuda.current_stream()
+    K = len(KINDS)
     barrier()
     torch.cuda.synchronize()
-    lib.mt_prof_begin(8192)
+    lib.mt_prof_begin(65536)
     l0 = lib.mt_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     results = []
     with clocks:
         e0.record(st)
-        for _ in range(args.steps):
-            ev.launch(theta)
-            results.append(ev.finish())
+        for s in range(args.steps):
+            results.append(run_eval(ev, theta, chol_events=cev[s]))
         e1.record(st)
         torch.cuda.synchronize()
     launches = lib.mt_launch_count() - l0
-    import ctypes
-    K = len(KINDS)
     arr = [(ctypes.c_double * K)() for _ in range(3)]
     cnt = (ctypes.c_int64 * K)()
     lib.mt_prof_end(K, arr[0], arr[1], arr[2], cnt)
     barrier()
     t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    value = args.steps * world / t_dev
+    t_chol = max_over_ranks(sum(a.elapsed_time(b) for a, b in cev) / 1e3 / args.steps)
+    value = args.steps / t_dev
+    chol_tflops = (n ** 3 / 3.0) / t_chol / 1e12
     kinds = {KINDS[q]: {"ms": arr[0][q] / args.steps, "flops": arr[1][q] / args.steps,
                         "bytes": arr[2][q] / args.steps, "launches": cnt[q] // max(1, args.steps)}
              for q in range(K)}
-    chol_ms = sum(kinds[k]["ms"] for k in ("potrf", "trsm64", "trsm32", "upd64", "upd32"))
 
-    # Cholesky-only device time (one extra pass, events around mt_cholesky)
-    m = ev.matrix
-    th = _lib.matern_struct(*THETA)
-    sh = _lib.stream_handle()
-    m.reset_status()
-    lib.mt_generate(ctypes.byref(m.desc), _lib.ptr(asm.d_locs), 0, 0.0, ctypes.byref(th), sh)
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    c0.record(st)
-    lib.mt_cholesky(ctypes.byref(m.desc), 1, sh)
-    c1.record(st)
-    torch.cuda.synchronize()
-    t_chol = max_over_ranks(c0.elapsed_time(c1) / 1e3)
-    chol_tflops = world * (n ** 3 / 3.0) / t_chol / 1e12
+    # ---- roofline of the dominant kernel, live in the timed region
+    peaks, peak_src = load_peaks()
+    bf16_sus = float(peaks.get("bf16_tflops_sustained") or FALLBACK_PEAKS["bf16_tflops_sustained"])
+    dom = "upd32"
+    d = kinds[dom]
+    achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
+    p32 = bf16_sus / 6.0  # tcgen05 kind::tf32 = bf16 rate / 2; 3xTF32 = 3 MMAs per FP32 product
+    p64c = ctypes.c_double()
+    lib.mt_peak_probe(2, 20000, ctypes.byref(p64c))
+    p64 = max_over_ranks(p64c.value) if dist_on else p64c.value
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        key = f"n{n}_nb{nb}_t{t}"
+        if key in tr and "tc32_update_kernel" in tr[key]:
+            traffic = tr[key]["tc32_update_kernel"]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
+    fl_plan = mt.planned_flops(n, nb, mp_pol)
+    t_roof = (fl_plan.sp / (p32 * 1e12) + fl_plan.dp / (p64 * 1e12)) / world
+    roofline = {
+        "bound": "tensor", "achieved": achieved, "peak": p32, "unit": "TFLOP/s",
+        "frac": achieved / p32, "traffic": traffic,
+        "kernel": "tc32_update_kernel",
+        "pipe": "tcgen05.mma kind::tf32 (3xTF32 FP32 emulation), TMEM accumulators, TMA",
+        "peak_source": (f"{peak_src}: bf16_tflops_sustained {bf16_sus:.0f} / 2 (TF32 rate) / 3 "
+                        "(MMAs per FP32 product); sustained figure since the kernel runs inside "
+                        "a long step"),
+        "launches_per_step": d["launches"],
+        "avg_launch_ms": d["ms"] / max(1, d["launches"]),
+        "algorithmic_flops_per_launch": d["flops"] / max(1, d["launches"]),
+        "measured": ("CUDA events on the launching stream around every bulk trailing-update "
+                     "launch inside the timed region (lookahead pipeline live); algorithmic "
+                     "flops = reference flop model (factor.py:83-95) per launch"),
+        "share_of_step": d["ms"] / (t_dev / args.steps * 1e3),
+        "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
+        "cholesky_flop_weighted": {
+            "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
+            "f_sp": fl_plan.sp, "f_dp": fl_plan.dp,
+            "p32_tflops": p32, "p64_tflops": p64,
+            "p32_source": "bf16_sustained/6 (3xTF32 on tcgen05)",
+            "p64_source": "mt_peak_probe: FP64 DMMA m8n8k4 chains on all SMs, this run"},
+    }
 
-    # Roofline pass: the same factorization with lookahead 0, so every event
-    # pair on the launching stream brackets exactly one kernel group (with the
-    # panel stream overlapping, event spans would include queueing time).
-    m.reset_status()
-    lib.mt_generate(ctypes.byref(m.desc), _lib.ptr(asm.d_locs), 0, 0.0, ctypes.byref(th), sh)
-    torch.cuda.synchronize()
-    lib.mt_prof_begin(8192)
-    lib.mt_cholesky(ctypes.byref(m.desc), 0, sh)
-    torch.cuda.synchronize()
-    ser = [(ctypes.c_double * K)() for _ in range(3)]
-    scnt = (ctypes.c_int64 * K)()
-    lib.mt_prof_end(K, ser[0], ser[1], ser[2], scnt)
-    serial = {KINDS[q]: {"ms": ser[0][q], "flops": ser[1][q], "bytes": ser[2][q],
-                         "launches": int(scnt[q])} for q in range(K)}
-    m.reset_status()
-    del m, ev  # free the MP pools before the DP / e2e legs (N=262144 MP needs ~145 GB)
-    import gc
-    gc.collect()
-    torch.cuda.empty_cache()
-
-    # ---- full-DP leg (the build's own full-DP path)
-    dp = None
-    p_tiles = -(-n // nb)
-    dp_bytes = p_tiles * (p_tiles + 1) // 2 * nb * nb * 8
-    free_bytes = torch.cuda.mem_get_info()[0]
-    if not args.no_dp and dp_bytes > 0.9 * free_bytes:
-        dp = {"skipped": f"full-DP tiles need {dp_bytes / 1e9:.0f} GB > free "
-                         f"{free_bytes / 1e9:.0f} GB on one GPU (needs the multi-GPU path)"}
-    elif not args.no_dp:
-        evd = mt.Evaluator(asm, mt.PrecisionPolicy.dp())
-        evd(theta)
-        barrier()
-        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        d0.record(st)
-        for _ in range(args.dp_steps):
-            evd(theta)
-        d1.record(st)
-        torch.cuda.synchronize()
-        t_dp = max_over_ranks(d0.elapsed_time(d1) / 1e3) / args.dp_steps
-        dp = {"evals_per_s": world / t_dp, "ms_per_eval": t_dp * 1e3,
-              "mp_speedup": (world / t_dp and (value / (world / t_dp)))}
-        del evd
-        torch.cuda.empty_cache()
-
-    # ---- e2e through the public API from host buffers
+    # ---- e2e through the public API from host buffers (pools of the timed
+    #      evaluator freed first: MP at N=262144 needs ~145 GB)
+    del ev
+    _free_memory()
     e2e = None
     if not args.no_e2e:
-        pin_locs = torch.from_numpy(np.ascontiguousarray(ds.locations)).pin_memory()
-        pin_z = torch.from_numpy(np.ascontiguousarray(ds.z)).pin_memory()
+        pin_locs = torch.from_numpy(np.array(ds.locations)).pin_memory()
+        pin_z = torch.from_numpy(np.array(ds.z)).pin_memory()
         host_ds = mt.GeoDataset(pin_locs.numpy(), pin_z.numpy())
-        mt.loglik(host_ds, theta, nb, mp_pol)  # warm the allocator
+
+        def api_call():
+            if dist_on:
+                return loglik_distributed(host_ds, theta, nb, mp_pol)
+            return mt.loglik(host_ds, theta, nb, mp_pol)
+
+        k_e2e = max(1, min(args.steps, 2))
         barrier()
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k_e2e = max(1, min(args.steps, 3))
         s0.record(st)
         for _ in range(k_e2e):
-            out = mt.loglik(host_ds, theta, nb, mp_pol)
+            out = api_call()
         s1.record(st)
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(s0.elapsed_time(s1) / 1e3)
-        e2e = {"value": k_e2e * world / t_e2e, "unit": UNIT,
+        e2e = {"value": k_e2e / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": int(ds.locations.nbytes + ds.z.nbytes),
                "d2h_bytes_per_step": 16 + 32 + 32,
-               "api": "paper_2003_05324_b200.loglik(dataset, params, nb, policy)",
+               "api": ("paper_2003_05324_b200.distributed.loglik_distributed"
+                       if dist_on else "paper_2003_05324_b200.loglik") +
+                      "(dataset, params, nb, policy)",
                "loglik": out.value}
+        _free_memory()
 
-    # ---- roofline of the dominant kernel (from the serialized pass)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    bf16_sus = peaks.get("bf16_tflops_sustained")
-    dom = max(("upd32", "upd64", "potrf", "trsm64", "trsm32", "gen32", "gen64"),
-              key=lambda k: serial[k]["ms"])
-    d = serial[dom]
-    achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
-    pk = ctypes.c_double()
-    if dom == "upd32" and bf16_sus:
-        # tcgen05 kind::tf32 runs at half the bf16 rate; 3xTF32 issues 3 MMAs
-        # per FP32 product -> algorithmic FP32 peak = bf16 / 2 / 3
-        peak = bf16_sus / 2.0 / 3.0
-        pipe = "tcgen05 kind::tf32 (3xTF32 FP32 emulation), TMEM accumulators"
-        src = ("MEASURED_PEAKS.json bf16_tflops_sustained / 2 (TF32 rate) / 3 (MMAs per FP32 "
-               "product); sustained figure since the kernel runs inside a long step")
-    else:
-        lib.mt_peak_probe(2 if dom in ("upd64", "potrf", "trsm64") else 0, 20000, ctypes.byref(pk))
-        peak = pk.value
-        pipe = "FP64 DMMA" if dom in ("upd64", "potrf", "trsm64") else "FP32 FFMA"
-        src = "measured this run by mt_peak_probe (MEASURED_PEAKS.json has no FP64/FFMA figure)"
-    traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof_path):
-        try:
-            traffic = json.load(open(prof_path)).get(dom)
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak if peak else None, "traffic": traffic,
-                "kernel": {"upd32": "tc32_update_kernel", "upd64": "dmma_update_kernel"}.get(dom, dom),
-                "pipe": pipe, "peak_source": src,
-                "launches_per_step": d["launches"],
-                "avg_launch_ms": d["ms"] / max(1, d["launches"]),
-                "measured": ("CUDA events around every launch of a lookahead-0 (serialized) "
-                             "factorization inside bench.py; algorithmic flops = reference "
-                             "flop model (factor.py:83-95) per launch"),
-                "share_of_serialized_cholesky": d["ms"] / max(1e-9, sum(v["ms"] for v in serial.values())),
-                "serialized_kernels": {k: {"ms": round(v["ms"], 2), "launches": v["launches"],
-                                           "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 2)}
-                                       for k, v in serial.items() if v["launches"]}}
-    # flop-weighted roofline of the whole factorization
-    fl_plan = mt.planned_flops(n, nb, mp_pol)
-    p64 = ctypes.c_double()
-    lib.mt_peak_probe(2, 20000, ctypes.byref(p64))
-    p32 = (bf16_sus / 6.0) if bf16_sus else None
-    if p32:
-        t_roof = fl_plan.sp / (p32 * 1e12) + fl_plan.dp / (p64.value * 1e12)
-        roofline["cholesky_flop_weighted"] = {
-            "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
-            "p32_tflops": p32, "p64_tflops": p64.value,
-            "p32_source": "bf16_sustained/6 (3xTF32)", "p64_source": "mt_peak_probe DMMA"}
+    # ---- the build's own full-DP path
+    dp = None
+    if not args.no_dp:
+        p_tiles = -(-n // nb)
+        dp_bytes = p_tiles * (p_tiles + 1) // 2 * nb * nb * 8 / world
+        free_bytes = torch.cuda.mem_get_info()[0]
+        free_min = -max_over_ranks(-float(free_bytes)) if dist_on else free_bytes
+        if dp_bytes < 0.9 * free_min:
+            dn, dt, dasm, mp_ref = n, t, asm, value
+        else:
+            dn, dt = args.dp_n, args.dp_t
+            dasm = mt.TileAssembler(_dataset(mt, dn), nb)
+            evm = make_eval(dasm, mt.PrecisionPolicy.mp(diag_thick=dt))
+            run_eval(evm, theta)
+            barrier()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(st)
+            for _ in range(3):
+                run_eval(evm, theta)
+            a1.record(st)
+            torch.cuda.synchronize()
+            mp_ref = 3 / max_over_ranks(a0.elapsed_time(a1) / 1e3)
+            del evm
+            _free_memory()
+        evd = make_eval(dasm, mt.PrecisionPolicy.dp())
+        if dn != n:
+            run_eval(evd, theta)  # warm (cheap at the reduced size)
+        barrier()
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record(st)
+        run_eval(evd, theta)
+        d1.record(st)
+        torch.cuda.synchronize()
+        t_dp = max_over_ranks(d0.elapsed_time(d1) / 1e3)
+        dp = {"n": dn, "mp_band_t": dt, "dp_evals_per_s": 1.0 / t_dp, "dp_ms_per_eval": t_dp * 1e3,
+              "mp_evals_per_s": mp_ref, "mp_speedup": mp_ref * t_dp,
+              "note": ("same N as the headline" if dn == n else
+                       f"full DP at N={n} needs {dp_bytes * world / 1e9:.0f} GB > "
+                       f"{world} GPU(s): compared at configs[1] N={dn}")}
+        del evd
+        _free_memory()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_obj(args)
 
     if rank == 0:
-        fl = mt.planned_flops(n, nb, mp_pol)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(3, args.warmup),
+            "steps": args.steps, "warmup": warm,
             "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[1]: N={n}, tile {nb}, MP band t={t}, "
-                                   f"Matern{THETA}, one loglik eval per step",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+            "config": {"workload": f"BASELINE metric config: N={n}, tile {nb}, MP band t={t}, "
+                                   f"Matern{THETA}, one loglik evaluation per step",
                        "n": n, "nb": nb, "band_t": t, "theta": list(THETA),
-                       "sp_flop_fraction": fl.sp_fraction,
-                       "l2": "inputs (tile pools) >> 126 MB L2; no flush needed",
+                       "sp_flop_fraction": fl_plan.sp_fraction,
+                       "l2": "inputs (tile pools, >= 35 GB) >> 126 MB L2; no flush needed",
                        "z": "N(0,1) timing-only observations (parity runs use field z)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": (f"tile-column-cyclic 1x{world}, NCCL panel broadcast"
+                                       if dist_on else "1 GPU")},
             "cholesky_tflops": chol_tflops, "cholesky_ms": t_chol * 1e3,
             # per-kind event spans inside the timed region; panel-stream spans
-            # include queueing behind the bulk update (true durations: roofline)
+            # include waiting for SMs held by the bulk update
             "kernel_event_spans_ms_per_step": {k: round(v["ms"], 3) for k, v in kinds.items()},
             "mp_vs_dp": dp, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "clocks": clocks.summary(),
@@ -431,7 +462,7 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

@@ -149,7 +149,9 @@ int mt_prof_start(int kind, cudaStream_t st, double flops, double bytes);
 void mt_prof_stop(int token, cudaStream_t st);
 enum MtKind {
   MT_K_GEN64 = 0, MT_K_GEN32, MT_K_POTRF, MT_K_TRSM64, MT_K_TRSM32, MT_K_UPD64, MT_K_UPD32,
-  MT_K_SOLVE, MT_K_MISC, MT_NKINDS
+  MT_K_SOLVE, MT_K_MISC,
+  MT_K_UPD64P, MT_K_UPD32P,  // lookahead panel-column updates (step k -> column k+1)
+  MT_NKINDS
 };
 // brackets the launches of one kernel group with profiling events
 struct ProfScope {

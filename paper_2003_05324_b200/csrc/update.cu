@@ -398,10 +398,11 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   }
   double f64, f32;
   update_flops(g, k, jlo, jhi, f64, f32);
+  const bool pcol = (jlo == k + 1 && jhi == jlo + 1 && jhi < g.p);  // lookahead panel column
   // band (FP64) outputs in columns [jlo, jhi)
   const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
   if (bcnt > 0) {
-    ProfScope ps(MT_K_UPD64, st, f64, bcnt * (double)nb * nb * 8.0 * 3.0);
+    ProfScope ps(pcol ? MT_K_UPD64P : MT_K_UPD64, st, f64, bcnt * (double)nb * nb * 8.0 * 3.0);
     if (nb % MBM == 0) {
       const int nsm = nb / MBM, nsn = nb / MBN;
       cudaFuncSetAttribute(dmma_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -419,7 +420,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   if (g.mode != MT_MODE_MP) return MT_OK;
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
   if (scnt > 0) {
-    ProfScope ps(MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
+    ProfScope ps(pcol ? MT_K_UPD32P : MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
     if ((mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) && mt_tc_supported(g)) {
       // the panel-column update (jhi == jlo + 1) runs beside the bulk update:
       // keep it narrow; the bulk update may be capped to leave SMs for the panel

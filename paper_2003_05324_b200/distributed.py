@@ -151,13 +151,18 @@ class DistributedEvaluator:
                                 _lib.ptr(self.out), st), "mt_sumsq")
         return float(self.out.item())
 
-    def __call__(self, params):
-        """(logdet, quad) of one evaluation; same values on every rank."""
+    def __call__(self, params, chol_events=None):
+        """(logdet, quad) of one evaluation; same values on every rank.
+        chol_events: optional (start, end) CUDA events around the factorization."""
         m = self.matrix
         m.reset_status()
         m.factored = False
         self.asm.generate_into(m, params)
+        if chol_events is not None:
+            chol_events[0].record()
         self.factor()
+        if chol_events is not None:
+            chol_events[1].record()
         bad, ov = self.status()
         if ov:
             raise PrecisionOverflowError(f"{ov} value(s) exceed FP32 range during narrowing")

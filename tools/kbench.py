@@ -12,7 +12,7 @@ ap.add_argument("--t", type=int, default=2); ap.add_argument("--dp", action="sto
 ap.add_argument("--lookahead", type=int, default=0); ap.add_argument("--engine", default="tf32x3")
 a = ap.parse_args()
 mt.set_fp32_engine(a.engine)
-KINDS = ["gen64", "gen32", "potrf", "trsm64", "trsm32", "upd64", "upd32", "solve", "misc"]
+KINDS = ["gen64", "gen32", "potrf", "trsm64", "trsm32", "upd64", "upd32", "solve", "misc", "upd64p", "upd32p"]
 locs = mt.generate_locations(a.n, seed=1)
 ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(a.n)))
 pol = mt.PrecisionPolicy.dp() if a.dp else mt.PrecisionPolicy.mp(diag_thick=a.t)
