@@ -54,7 +54,10 @@ extern "C" {
  *   status:  int64[4] device: [0] first failing global pivot (-1 = none),
  *            [1] FP32 narrowing overflow count, [2] duplicate-location pairs.
  *   split:   TF32 hi/lo split of panels k (ring of 2): tile (i, k) of panel k at
- *            split + ((k&1)*p + i)*2*nb*nb (hi) and + nb*nb (lo).
+ *            split + ((k&1)*p + i)*2*nb*nb (hi) and + nb*nb (lo); then the
+ *            pre-TRSM split of the next panel's off-band tiles at
+ *            split + (4p + 2i)*nb*nb, and the split of W = L_kk^{-1} (row-major)
+ *            at split + 6p*nb*nb (hi) / + nb*nb (lo): 6p + 2 tiles in all.
  */
 typedef struct mt_tiles {
   int64_t n;
@@ -214,7 +217,10 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
 
 /* Runtime options; returns the previous value.
  *   0: FP32 (off-band) update engine: 0 = SIMT FFMA, 1 = tcgen05 3xTF32 (default)
- *   1: CTA cap of the bulk trailing update (0 = all SMs) */
+ *   1: CTA cap of the bulk trailing update (0 = all SMs)
+ *   2: 1 = register-staged DMMA band update instead of the TMA-staged one
+ *   3: off-band panel TRSM: 1 = tcgen05 3xTF32 GEMM against L_kk^{-1} (default),
+ *      0 = SIMT blocked substitution against 32x32 diagonal-block inverses */
 int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */

@@ -91,6 +91,14 @@ struct Grid {
     return split + ((int64_t)(k & 1) * p + i) * 2 * tile_elems();
   }
   MT_HD float* split_lo(int i, int k) const { return split_hi(i, k) + tile_elems(); }
+  // split buffer tail (tensor-core TRSM): the pre-TRSM split of the next
+  // panel's off-band tiles (written by the update epilogue into column k+1)
+  // and the split of W = L_kk^{-1} (row-major), one slot each
+  MT_HD int64_t presplit_row(int i) const { return ((int64_t)4 * p + 2 * i) * nb; }
+  MT_HD int64_t winv_row() const { return (int64_t)6 * p * nb; }
+  MT_HD float* presplit_hi(int i) const { return split + presplit_row(i) * nb; }
+  MT_HD float* winv_hi() const { return split + winv_row() * nb; }
+  MT_HD float* winv_lo() const { return winv_hi() + tile_elems(); }
   MT_HD float* smirror(int i, int k) const { return sdiag(k) + (int64_t)(i - k) * tile_elems(); }
   // FP32 operand for tile (i,k) of panel k in an FP32 update: payload or mirror
   MT_HD const float* sp_operand(int i, int k) const {
@@ -168,5 +176,11 @@ struct ProfScope {
 enum MtEngine { MT_ENGINE_FFMA = 0, MT_ENGINE_TF32X3 = 1 };
 int mt_opt_engine();
 int mt_opt_update_ctas();
+int mt_opt_legacy_dmma();
+bool mt_dmma_tma_supported(const Grid& g);
+int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st);
 bool mt_tc_supported(const Grid& g);
+bool mt_tc_trsm_enabled(const Grid& g);  // off-band TRSM as a tcgen05 GEMM against L_kk^{-1}
+int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st);
+int mt_opt_tc_trsm();
 int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st);

@@ -25,9 +25,10 @@
 // ascending k: deterministic, schedule-invariant.
 #include <cuda.h>
 
-#include "mt_grid.cuh"
+#include "tma.cuh"
 
 namespace {
+using namespace mt_tma;
 
 constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 4;          // 8 KB
@@ -38,39 +39,6 @@ constexpr int EPI_STRIDE = 33;                        // transpose tile, conflic
 constexpr int EPI_BYTES = 4 * 32 * EPI_STRIDE * 4;    // 4 warps x 32x33 floats
 constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-      "%4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 // K-major, SWIZZLE_64B smem matrix descriptor (8-row atoms of 64 B, SBO = 512 B)
 __device__ __forceinline__ uint64_t sw64_desc(const void* p) {
   const uint64_t a = (smem_u32(p) >> 4) & 0x3FFF;
@@ -97,13 +65,18 @@ struct Work {
   int nitems;  // slots * nsub
   int nsubm, nsubn;
   int* counter;  // dynamic work queue head (zeroed before the launch)
+  int presplit;  // update: also write the pre-TRSM split of column k+1 outputs
 };
 
 constexpr int SCHED = 4;  // work-item ring between the producer and the consumers
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    tc32_update_kernel(Grid g, int k, Work w, const __grid_constant__ CUtensorMap map_a,
-                       const __grid_constant__ CUtensorMap map_b) {
+// TRSM = false: C_ij -= A_ik A_jk^T (trailing update of step k)
+// TRSM = true:  X_ik = B_ik W^T, W = L_kk^{-1} (off-band panel solve of step k):
+//               A rows from the pre-split of B, B rows from the split of W; W is
+//               lower triangular, so output columns [n0, n0 + 256) need K < n0 + 256
+template <bool TRSM>
+__device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
+                                          const CUtensorMap& map_a, const CUtensorMap& map_b) {
   if (g.failed()) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
@@ -120,8 +93,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = g.nb;
-  const int ksteps = nb / BK;
   const int nsub = w.nsubm * w.nsubn;
+  auto item_ksteps = [&](int item) {
+    return TRSM ? ((item % nsub) % w.nsubn + 1) * (BN / BK) : nb / BK;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -180,9 +155,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (item < 0) break;
         int i, j, m0, n0;
         item_ij(item, i, j, m0, n0);
-        // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb
-        const int arow = ((k & 1) * g.p + i) * 2 * nb + m0;
-        const int brow = ((k & 1) * g.p + j) * 2 * nb + n0;
+        // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb;
+        // TRSM: A = pre-split of B_ik, B = split of W = L_kk^{-1}
+        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
+        const int brow = TRSM ? (int)g.winv_row() + n0 : ((k & 1) * g.p + j) * 2 * nb + n0;
+        const int ksteps = item_ksteps(item);
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -200,7 +177,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------ MMA issuer
     uint32_t it = 0;
     for (uint32_t li = 0;; ++li) {
-      if (next_item(li) < 0) break;
+      const int item = next_item(li);
+      if (item < 0) break;
+      const int ksteps = item_ksteps(item);
       const uint32_t b = li & 1, aph = (li >> 1) & 1;
       mbar_wait(&tempty[b], aph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -243,7 +222,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
       // rows q*32 .. q*32+31 of the 128x256 item; lane owns row q*32+lane in TMEM
-      float* cbase = g.stile(i, j) + (int64_t)(m0 + q * 32) * nb + n0;
+      const int64_t roff = (int64_t)(m0 + q * 32) * nb + n0;
+      float* cbase = g.stile(i, j) + roff;
+      // split outputs: TRSM -> the panel split read by this step's updates;
+      // update of column k+1 -> the pre-TRSM split of the next panel
+      float* shi = TRSM ? g.split_hi(i, k) + roff
+                        : ((w.presplit && j == k + 1) ? g.presplit_hi(i) + roff : nullptr);
+      const int64_t te = g.tile_elems();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -263,12 +248,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 32; ++u) stg[lane * EPI_STRIDE + u] = __uint_as_float(v[u]);
         __syncwarp();
-        float cv[32];
         float* cp = cbase + c + lane;
+        float* hp = shi ? shi + c + lane : nullptr;
 #pragma unroll
-        for (int r = 0; r < 32; ++r) cv[r] = cp[(int64_t)r * nb];
+        for (int r0 = 0; r0 < 32; r0 += 16) {  // 16 rows in flight per lane
+          float cv[16];
+          if (TRSM) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) cp[(int64_t)r * nb] = cv[r] - stg[r * EPI_STRIDE + lane];
+            for (int r = 0; r < 16; ++r) cv[r] = stg[(r0 + r) * EPI_STRIDE + lane];
+          } else {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) cv[r] = cp[(int64_t)(r0 + r) * nb];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) cv[r] -= stg[(r0 + r) * EPI_STRIDE + lane];
+          }
+#pragma unroll
+          for (int r = 0; r < 16; ++r) cp[(int64_t)(r0 + r) * nb] = cv[r];
+          if (hp) {
+            float* hrow = hp + (int64_t)r0 * nb;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+              uint32_t h;
+              asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(cv[r]));
+              asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(__uint_as_float(h)) : "memory");
+              asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(cv[r] - __uint_as_float(h))
+                           : "memory");
+              hrow += nb;
+            }
+          }
+        }
         __syncwarp();
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -284,13 +292,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc32_update_kernel(Grid g, int k, Work w, const __grid_constant__ CUtensorMap map_a,
+                       const __grid_constant__ CUtensorMap map_b) {
+  tc32_body<false>(g, k, w, map_a, map_b);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc32_trsm_kernel(Grid g, int k, Work w, const __grid_constant__ CUtensorMap map_a,
+                     const __grid_constant__ CUtensorMap map_b) {
+  tc32_body<true>(g, k, w, map_a, map_b);
+}
+
 // ------------------------------------------------------------- host side
+int make_map(CUtensorMap* m, const float* base, int64_t rows, int nb, int box_rows) {
+  return make_map_2d(m, base, rows, nb, 4, BK, box_rows, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+int g_sm_count = 0;
+
+}  // namespace
+
+namespace mt_tma {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-EncodeTiledFn encode_fn() {
+static EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -303,15 +332,16 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int make_map(CUtensorMap* m, const float* base, int64_t rows, int nb, int box_rows) {
+int make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int es,
+                int box_cols, int box_rows, CUtensorMapSwizzle swz) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) { mt_set_error("cuTensorMapEncodeTiled unavailable"); return MT_E_CUDA; }
-  cuuint64_t dims[2] = {(cuuint64_t)nb, (cuuint64_t)(rows > 0 ? rows : 1)};
-  cuuint64_t strides[1] = {(cuuint64_t)nb * 4};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * es};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                  2, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     mt_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -319,21 +349,25 @@ int make_map(CUtensorMap* m, const float* base, int64_t rows, int nb, int box_ro
   }
   return MT_OK;
 }
-
-int g_sm_count = 0;
-
-}  // namespace
+}  // namespace mt_tma
 
 bool mt_tc_supported(const Grid& g) {
   return g.mode == MT_MODE_MP && g.split != nullptr && g.nb % BN == 0 &&
-         (int64_t)4 * g.p * g.nb < (1ll << 31);
+         ((int64_t)6 * g.p + 2) * g.nb < (1ll << 31);
 }
 
-// FP32 updates of step k into off-band slots [s0, s0+scnt) via tcgen05; `ctas` caps the grid.
-int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st) {
+bool mt_tc_trsm_enabled(const Grid& g) {
+  return mt_opt_tc_trsm() && (mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) &&
+         mt_tc_supported(g);
+}
+
+namespace {
+// persistent launch over `nitems` work items of slot range [s0, s0 + scnt)
+int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
+                cudaStream_t st) {
   if (scnt <= 0) return MT_OK;
   CUtensorMap ma, mb;
-  const int64_t split_rows = (int64_t)4 * g.p * g.nb;  // 2 panels x p tiles x {hi, lo}
+  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;  // whole split buffer
   int rc = make_map(&ma, g.split, split_rows, g.nb, BM);
   if (!rc) rc = make_map(&mb, g.split, split_rows, g.nb, BN);
   if (rc) return rc;
@@ -342,6 +376,7 @@ int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, 
   w.nsubm = g.nb / BM;
   w.nsubn = g.nb / BN;
   w.nitems = (int)(scnt * w.nsubm * w.nsubn);
+  w.presplit = (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_sm_count) cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -357,8 +392,33 @@ int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, 
   int grid = ctas > 0 ? ctas : g_sm_count;
   if (grid > w.nitems) grid = w.nitems;
   const size_t smem = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
-  cudaFuncSetAttribute(tc32_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tc32_update_kernel<<<grid, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
-  MT_LAUNCH_CHECK("tc32_update_kernel");
+  if (trsm) {
+    cudaFuncSetAttribute(tc32_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tc32_trsm_kernel<<<grid, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+    MT_LAUNCH_CHECK("tc32_trsm_kernel");
+  } else {
+    cudaFuncSetAttribute(tc32_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tc32_update_kernel<<<grid, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+    MT_LAUNCH_CHECK("tc32_update_kernel");
+  }
   return MT_OK;
+}
+}  // namespace
+
+// FP32 updates of step k into off-band slots [s0, s0+scnt) via tcgen05; `ctas` caps the grid.
+int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st) {
+  return launch_tc32(g, k, s0, scnt, ctas, false, st);
+}
+
+// Off-band panel TRSM of step k: X_ik = B_ik W^T for the off-band rows of
+// column k, W = L_kk^{-1} split by trinv_kernel, B_ik pre-split by the update
+// epilogue of step k-1 (or presplit_kernel); writes X and its split.
+int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st) {
+  const int64_t s0 = g.scol(k), cnt = g.scol(k + 1) - s0;
+  if (cnt <= 0) return MT_OK;
+  // algorithmic work as the reference's strsm: rows(i) * rows(k)^2 per tile
+  const double nb = g.nb, rk = g.rows(k);
+  const double rows_sum = (cnt - 1) * nb + g.rows(g.p - 1);
+  ProfScope ps(MT_K_TRSM32, st, rows_sum * rk * rk, cnt * nb * nb * 4.0 * 5.0);
+  return launch_tc32(g, k, s0, cnt, 0, true, st);
 }

@@ -20,6 +20,9 @@
 // cp.async ring that runs ahead across column blocks.
 #include "mt_grid.cuh"
 
+#define RC_(call) \
+  do { int rc__ = (call); if (rc__) return rc__; } while (0)
+
 namespace {
 
 constexpr int kThreads = 256;  // 8 warps; lane = column of the 32-wide block
@@ -221,7 +224,114 @@ int launch_trsm(const Grid& g, int k, int64_t s0, int64_t cnt, int mirror_ok, cu
   return MT_OK;
 }
 
+// W = L_kk^{-1} (lower, FP64) for the tensor-core off-band TRSM X = B W^T.
+// CTA cb owns the 32-column block cb of W and walks its row blocks down:
+//   W[cb, cb] = Li_cb                      (published by POTRF)
+//   W[rb, cb] = -Li_rb sum_{m=cb}^{rb-1} L[rb, m] W[m, cb]
+// The result is written row-major as its FP32 rounding split into TF32
+// hi/lo (the operand format of the 3xTF32 UMMA), zeros above the diagonal.
+constexpr int WLD = 33;
+
+__global__ void __launch_bounds__(256) trinv_kernel(Grid g, int k) {
+  if (g.failed()) return;
+  const int nb = g.nb, nblk = nb / 32, cb = blockIdx.x;
+  const double* __restrict__ L = g.dtile(k, k);
+  const double* __restrict__ inv = g.sinv64(k);
+  extern __shared__ __align__(16) double wsm[];
+  double* Wc = wsm;                 // [nb][WLD]: column block cb of W
+  double* Tt = Wc + nb * WLD;       // [32][WLD]
+  const int tid = threadIdx.x, r = tid >> 3, c4 = (tid & 7) * 4;
+  for (int e = tid; e < 1024; e += 256) Wc[(cb * 32 + (e >> 5)) * WLD + (e & 31)] = inv[cb * 1024 + e];
+  __syncthreads();
+  for (int rb = cb + 1; rb < nblk; ++rb) {
+    // T = L[rb, cb:rb] W[cb:rb, cb]: L row read straight from L2 (8 threads
+    // share a row; no staging barriers on the dependent chain)
+    const double* lrow = L + (int64_t)(rb * 32 + r) * nb;
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int q = cb * 32; q < rb * 32; ++q) {
+      const double lv = __ldg(lrow + q);
+      const double* wr = Wc + q * WLD + c4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = fma(lv, wr[u], t[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Tt[r * WLD + c4 + u] = t[u];
+    __syncthreads();
+    const double* li = inv + rb * 1024 + r * 32;
+    double o[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double lv = __ldg(li + q);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = fma(lv, Tt[q * WLD + c4 + u], o[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Wc[(rb * 32 + r) * WLD + c4 + u] = -o[u];
+    __syncthreads();
+  }
+  float* WH = g.winv_hi();
+  float* WL = g.winv_lo();
+  for (int e = tid; e < nb * 32; e += 256) {
+    const int R = e >> 5, c = e & 31;
+    const double w = R >= cb * 32 ? Wc[R * WLD + c] : 0.0;
+    const float f = __double2float_rn(w);
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
+    const int64_t o = (int64_t)R * nb + cb * 32 + c;
+    WH[o] = __uint_as_float(h);
+    WL[o] = f - __uint_as_float(h);
+  }
+}
+
+// pre-TRSM split of panel k's off-band tiles (k = 0, or when no update
+// epilogue produced it): presplit(i) = {rna_tf32(x), x - hi}
+__global__ void __launch_bounds__(256) presplit_kernel(Grid g, int k, int64_t s0) {
+  const int64_t te = g.tile_elems();
+  const int64_t slot = s0 + blockIdx.y;
+  int i, j;
+  g.off_slot_ij(slot, i, j);
+  const float4* src = (const float4*)g.stile(i, k);
+  float4* hi = (float4*)g.presplit_hi(i);
+  float4* lo = (float4*)(g.presplit_hi(i) + te);
+  for (int64_t e = blockIdx.x * 256 + threadIdx.x; e < te / 4; e += (int64_t)gridDim.x * 256) {
+    const float4 x = src[e];
+    float4 h, l;
+    float* xp = (float*)&x;
+    float* hp = (float*)&h;
+    float* lp = (float*)&l;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t b;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(xp[u]));
+      hp[u] = __uint_as_float(b);
+      lp[u] = xp[u] - hp[u];
+    }
+    hi[e] = h;
+    lo[e] = l;
+  }
+}
+
 }  // namespace
+
+int mt_trinv_impl(const Grid& g, int k, cudaStream_t st) {
+  const size_t smem = ((size_t)g.nb * WLD + 32 * WLD) * sizeof(double);
+  cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const double nb = g.nb;
+  ProfScope ps(MT_K_MISC, st, nb * nb * nb / 3.0, nb * nb * 16.0);
+  trinv_kernel<<<g.nb / 32, 256, smem, st>>>(g, k);
+  MT_LAUNCH_CHECK("trinv_kernel");
+  return MT_OK;
+}
+
+int mt_presplit_impl(const Grid& g, int k, cudaStream_t st) {
+  const int64_t s0 = g.scol(k), cnt = g.scol(k + 1) - s0;
+  if (cnt <= 0) return MT_OK;
+  ProfScope ps(MT_K_MISC, st, 0.0, cnt * (double)g.tile_elems() * 12.0);
+  presplit_kernel<<<dim3(16, (unsigned)cnt), 256, 0, st>>>(g, k, s0);
+  MT_LAUNCH_CHECK("presplit_kernel");
+  return MT_OK;
+}
 
 // Panel rows i in (k, p) of tile column k.  Band rows: band slots
 // bcol(k)+1 .. bcol(k+1)-1; off-band rows: off slots scol(k) .. scol(k+1)-1.
@@ -232,7 +342,15 @@ int mt_trsm_impl(const Grid& g, int k, cudaStream_t st) {
   }
   int rc = launch_trsm<double, 32>(g, k, g.bcol(k) + 1, g.bcol(k + 1) - g.bcol(k) - 1, 1, st);
   if (rc) return rc;
-  if (g.mode == MT_MODE_MP)
-    rc = launch_trsm<float, 64>(g, k, g.scol(k), g.scol(k + 1) - g.scol(k), 0, st);
+  if (g.mode == MT_MODE_MP && g.scol(k + 1) > g.scol(k)) {
+    if (mt_tc_trsm_enabled(g)) {
+      // the update epilogue of step k-1 pre-split column k (k = 0: nobody did)
+      if (k == 0) RC_(mt_presplit_impl(g, k, st));
+      RC_(mt_trinv_impl(g, k, st));
+      rc = mt_tc_trsm_impl(g, k, st);
+    } else {
+      rc = launch_trsm<float, 64>(g, k, g.scol(k), g.scol(k + 1) - g.scol(k), 0, st);
+    }
+  }
   return rc;
 }

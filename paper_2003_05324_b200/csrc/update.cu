@@ -402,8 +402,11 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   // band (FP64) outputs in columns [jlo, jhi)
   const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
   if (bcnt > 0) {
+    int return_rc = MT_OK;
     ProfScope ps(pcol ? MT_K_UPD64P : MT_K_UPD64, st, f64, bcnt * (double)nb * nb * 8.0 * 3.0);
-    if (nb % MBM == 0) {
+    if (mt_opt_legacy_dmma() != 1 && mt_dmma_tma_supported(g)) {
+      return_rc = mt_dmma_update_impl(g, k, b0, bcnt, st);
+    } else if (nb % MBM == 0) {
       const int nsm = nb / MBM, nsn = nb / MBN;
       cudaFuncSetAttribute(dmma_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            MMA_SMEM);
@@ -415,6 +418,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
       const int nblk = (nb * nb + 255) / 256;
       gemm_generic_kernel<true><<<(unsigned)(bcnt * nblk), 256, 0, st>>>(g, k, b0, nblk);
     }
+    if (return_rc) return return_rc;
     MT_LAUNCH_CHECK("dgemm_update");
   }
   if (g.mode != MT_MODE_MP) return MT_OK;

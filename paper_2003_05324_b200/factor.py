@@ -235,6 +235,18 @@ def set_fp32_engine(name):
     return {v: k for k, v in _ENGINES.items()}[old]
 
 
+def set_legacy_dmma(flag):
+    """1: use the register-staged DMMA band update instead of the TMA-staged one
+    (A/B comparisons; both apply identical DMMA sequences). Returns the old flag."""
+    return _lib.load().mt_set_option(2, int(flag))
+
+
+def set_tc_trsm(flag):
+    """1 (default): off-band panel TRSM as a tcgen05 3xTF32 GEMM against
+    W = L_kk^{-1}; 0: SIMT blocked substitution. Returns the old flag."""
+    return _lib.load().mt_set_option(3, int(flag))
+
+
 def set_update_ctas(ctas):
     """Cap the CTAs of the bulk trailing update (0 = all SMs); returns the old cap."""
     return _lib.load().mt_set_option(1, int(ctas))

@@ -150,3 +150,20 @@ def test_evaluate_host_c_entry(gpu):
     want = g["results"]["mp:2"]
     assert math.isclose(out[0], want[1], rel_tol=1e-6)
     assert math.isclose(out[1], want[2], rel_tol=1e-5)
+
+
+def test_evaluator_split_launch_equals_fused(gpu):
+    """bench.py's timed step (generate / events / cholesky / logdet / quad as
+    separate calls) enqueues the same work as the fused mt_evaluate."""
+    import torch
+    mt = _mt()
+    g = load_golden("config1")
+    ds = mt.GeoDataset(g["locs"], g["z"])
+    ev = mt.Evaluator(mt.TileAssembler(ds, 256), mt.PrecisionPolicy.mp(diag_thick=2))
+    th = mt.MaternParams(1.0, 0.1, 0.5)
+    fused = ev(th)
+    e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev.launch(th, chol_events=e)
+    split = ev.finish()
+    assert split == fused
+    assert e[0].elapsed_time(e[1]) > 0.0

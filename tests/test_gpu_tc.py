@@ -93,3 +93,71 @@ def test_tf32x3_large_tile_512(engine):
     ev = mt.loglik(ds, mt.MaternParams(*theta), nb, mt.PrecisionPolicy.mp(diag_thick=t))
     want, _, _ = O.loglik(ds.locations, ds.z, theta, nb, "mp", t)
     assert abs(ev.value - want) / abs(want) <= 1e-5
+
+
+@pytest.mark.parametrize("mode,t", [("dp", None), ("mp", 2), ("mp", 3)])
+def test_tma_dmma_update_bitwise_equals_register_staged(gpu, mode, t):
+    """The TMA-staged DMMA band update applies the same DMMA sequence per
+    output element as the register-staged kernel: factors are bitwise equal."""
+    mt = _mt()
+    n, nb = 1920, 256  # ragged last tile row
+    theta = (1.0, 0.1, 0.5)
+    locs = mt.generate_locations(n, seed=5)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    pol = mt.PrecisionPolicy.dp() if mode == "dp" else mt.PrecisionPolicy.mp(diag_thick=t)
+    facs = []
+    for legacy in (0, 1):
+        old = mt.set_legacy_dmma(legacy)
+        try:
+            facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(*theta), nb, pol)))
+        finally:
+            mt.set_legacy_dmma(old)
+    a, b = facs
+    for key in a.tiles:
+        ta, tb = a.tiles[key], b.tiles[key]
+        if ta.dp is not None and tb.dp is not None and a.matrix.band(*key):
+            assert np.array_equal(ta.dp, tb.dp), key
+
+
+@pytest.mark.parametrize("n,nb,t", [(2048, 256, 2), (2000, 256, 1), (3072, 512, 2)])
+def test_tc_trsm_matches_substitution_and_oracle(engine, n, nb, t):
+    """Off-band TRSM as a 3xTF32 GEMM against L_kk^{-1}: FP32-class accuracy,
+    within a small factor of the SIMT substitution, ragged last tile included."""
+    mt = engine
+    theta = (1.0, 0.1, 0.5)
+    locs = mt.generate_locations(n, seed=11)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    ref = O.cholesky(O.assemble(ds.locations, theta, nb, "mp", t), n, nb, "mp", t)
+    facs = {}
+    for flag in (1, 0):
+        old = mt.set_tc_trsm(flag)
+        try:
+            facs[flag] = _factor(mt, ds, theta, nb, t, "tf32x3")
+        finally:
+            mt.set_tc_trsm(old)
+    errs = {}
+    for flag, f in facs.items():
+        e = 0.0
+        for key, (dp, _) in ref.items():
+            e = max(e, float(np.max(np.abs(f.tiles[key].dp - dp))))
+        errs[flag] = e
+    assert errs[1] < 5e-5 and errs[0] < 5e-5, errs
+    assert errs[1] <= 8.0 * errs[0] + 1e-7, errs
+
+
+def test_tc_trsm_loglik_parity_strong_field(engine):
+    """Strong-correlation field (beta=0.3, nu=1): the ill-conditioned case for
+    an inverse-based solve; the MP tolerance vs the reference must still hold."""
+    mt = engine
+    g = load_golden("strong1024")
+    ds = mt.GeoDataset(g["locs"], g["z"])
+    theta = tuple(float(v) for v in g["theta"])
+    nb, t = 256, 1
+    ref, _, _ = O.loglik(ds.locations, ds.z, theta, nb, "mp", t)
+    for flag in (1, 0):
+        old = mt.set_tc_trsm(flag)
+        try:
+            ev = mt.loglik(ds, mt.MaternParams(*theta), nb, mt.PrecisionPolicy.mp(diag_thick=t))
+        finally:
+            mt.set_tc_trsm(old)
+        assert abs(ev.value - ref) / abs(ref) < 2e-4, (flag, ev.value, ref)
