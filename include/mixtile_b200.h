@@ -220,7 +220,8 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   1: CTA cap of the bulk trailing update (0 = all SMs)
  *   2: 1 = register-staged DMMA band update instead of the TMA-staged one
  *   3: off-band panel TRSM: 1 = tcgen05 3xTF32 GEMM against L_kk^{-1} (default),
- *      0 = SIMT blocked substitution against 32x32 diagonal-block inverses */
+ *      0 = SIMT blocked substitution against 32x32 diagonal-block inverses
+ *   4: CTAs of the lookahead panel-column FP32 update (0 = all SMs) */
 int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */

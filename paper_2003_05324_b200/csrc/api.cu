@@ -184,11 +184,13 @@ double zeta_odd(int idx) {  // covmath.py:52-66 (sum k^-s, k < 60, + Euler-Macla
 static int g_engine = MT_ENGINE_TF32X3;
 static int g_update_ctas = 0;  // 0 = all SMs
 static int g_legacy_dmma = 0;  // 1 = register-staged DMMA band update (A/B comparisons)
+static int g_pcol_ctas = 64;   // CTAs of the lookahead panel-column FP32 update (0 = all SMs)
 static int g_tc_trsm = 1;      // 1 = off-band TRSM as a tcgen05 3xTF32 GEMM against L_kk^{-1}
 int mt_opt_engine() { return g_engine; }
 int mt_opt_update_ctas() { return g_update_ctas; }
 int mt_opt_legacy_dmma() { return g_legacy_dmma; }
 int mt_opt_tc_trsm() { return g_tc_trsm; }
+int mt_opt_pcol_ctas() { return g_pcol_ctas; }
 
 extern "C" {
 
@@ -198,13 +200,15 @@ int32_t mt_version(void) { return 11; }
  * option 1: CTA cap of the bulk trailing update (0 = all SMs);
  * option 2: 1 = legacy register-staged DMMA band update;
  * option 3: 1 = off-band TRSM as a tcgen05 GEMM against L_kk^{-1} (default),
- *           0 = SIMT substitution against 32x32 inverses. Returns old value. */
+ *           0 = SIMT substitution against 32x32 inverses;
+ * option 4: CTAs of the lookahead panel-column FP32 update (0 = all SMs). Returns old value. */
 int32_t mt_set_option(int32_t option, int32_t value) {
   int old = -1;
   if (option == 0) { old = g_engine; g_engine = value; }
   else if (option == 1) { old = g_update_ctas; g_update_ctas = value; }
   else if (option == 2) { old = g_legacy_dmma; g_legacy_dmma = value; }
   else if (option == 3) { old = g_tc_trsm; g_tc_trsm = value; }
+  else if (option == 4) { old = g_pcol_ctas; g_pcol_ctas = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

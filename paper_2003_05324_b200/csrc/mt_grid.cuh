@@ -177,6 +177,7 @@ enum MtEngine { MT_ENGINE_FFMA = 0, MT_ENGINE_TF32X3 = 1 };
 int mt_opt_engine();
 int mt_opt_update_ctas();
 int mt_opt_legacy_dmma();
+int mt_opt_pcol_ctas();
 bool mt_dmma_tma_supported(const Grid& g);
 int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st);
 bool mt_tc_supported(const Grid& g);

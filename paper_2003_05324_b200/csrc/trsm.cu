@@ -225,60 +225,121 @@ int launch_trsm(const Grid& g, int k, int64_t s0, int64_t cnt, int mirror_ok, cu
 }
 
 // W = L_kk^{-1} (lower, FP64) for the tensor-core off-band TRSM X = B W^T.
-// CTA cb owns the 32-column block cb of W and walks its row blocks down:
-//   W[cb, cb] = Li_cb                      (published by POTRF)
-//   W[rb, cb] = -Li_rb sum_{m=cb}^{rb-1} L[rb, m] W[m, cb]
-// The result is written row-major as its FP32 rounding split into TF32
-// hi/lo (the operand format of the 3xTF32 UMMA), zeros above the diagonal.
-constexpr int WLD = 33;
+// The columns of W are independent triangular solves L w_c = e_c, so CTA b
+// owns the 8 columns c0 = 8b .. c0+7 (64 CTAs at nb = 512: a short dependent
+// chain per CTA) and walks their 32-row blocks down:
+//   W[cb, cols] = Li_cb[:, cols]            (POTRF's diagonal-block inverse)
+//   W[rb, cols] = -Li_rb (L[rb, cb:rb] W[cb:rb, cols])
+// Both products run on DMMA (m8n8k4 f64, one 8 x 8 fragment per warp).  The L
+// row blocks and Li_rb do not depend on W: they stream through a 4-deep
+// cp.async ring of 32 x 64 chunks ahead of the dependent chain.  The result is
+// written row-major as its FP32 rounding split into TF32 hi/lo (the operand
+// format of the 3xTF32 UMMA), zeros above the diagonal.
+constexpr int TW = 8;     // columns of W per CTA
+constexpr int CW = 64;    // chunk width (columns of L)
+constexpr int CLD = 68;   // chunk row stride (doubles): 16-B rows, 2-wavefront fragments
+constexpr int NCH = 4;    // ring depth
 
-__global__ void __launch_bounds__(256) trinv_kernel(Grid g, int k) {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) trinv_kernel(Grid g, int k) {
   if (g.failed()) return;
-  const int nb = g.nb, nblk = nb / 32, cb = blockIdx.x;
+  const int nb = g.nb, nblk = nb / 32;
+  const int c0 = blockIdx.x * TW, cb = c0 / 32, cc0 = c0 % 32;
   const double* __restrict__ L = g.dtile(k, k);
   const double* __restrict__ inv = g.sinv64(k);
   extern __shared__ __align__(16) double wsm[];
-  double* Wc = wsm;                 // [nb][WLD]: column block cb of W
-  double* Tt = Wc + nb * WLD;       // [32][WLD]
-  const int tid = threadIdx.x, r = tid >> 3, c4 = (tid & 7) * 4;
-  for (int e = tid; e < 1024; e += 256) Wc[(cb * 32 + (e >> 5)) * WLD + (e & 31)] = inv[cb * 1024 + e];
-  __syncthreads();
-  for (int rb = cb + 1; rb < nblk; ++rb) {
-    // T = L[rb, cb:rb] W[cb:rb, cb]: L row read straight from L2 (8 threads
-    // share a row; no staging barriers on the dependent chain)
-    const double* lrow = L + (int64_t)(rb * 32 + r) * nb;
-    double t[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
-    for (int q = cb * 32; q < rb * 32; ++q) {
-      const double lv = __ldg(lrow + q);
-      const double* wr = Wc + q * WLD + c4;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) t[u] = fma(lv, wr[u], t[u]);
+  double* Wc = wsm;                 // [nb][TW]: columns c0.. of W (rows >= cb*32 used)
+  double* Tt = Wc + nb * TW;        // [32][TW]
+  double* ring = Tt + 32 * TW;      // [NCH][32][CLD]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+
+  // chunk sequence: for rb = cb+1.., L chunks q0 = cb*32, +64, .. < rb*32, then Li_rb
+  auto chunk_of = [&](int idx, int& rb, int& q0) {
+    for (rb = cb + 1; rb < nblk; ++rb) {
+      const int n = (rb - cb + 1) / 2 + 1;
+      if (idx < n) {
+        q0 = idx == n - 1 ? -1 : cb * 32 + idx * CW;
+        return true;
+      }
+      idx -= n;
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) Tt[r * WLD + c4 + u] = t[u];
-    __syncthreads();
-    const double* li = inv + rb * 1024 + r * 32;
-    double o[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
-    for (int q = 0; q < 32; ++q) {
-      const double lv = __ldg(li + q);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) o[u] = fma(lv, Tt[q * WLD + c4 + u], o[u]);
+    return false;
+  };
+  auto issue = [&](int idx) {
+    int rb, q0;
+    if (chunk_of(idx, rb, q0)) {
+      double* dst = ring + (idx % NCH) * 32 * CLD;
+      if (q0 < 0) {  // Li_rb, 32 x 32 row-major
+        for (int e = tid; e < 32 * 16; e += 128) {
+          const int rr = e >> 4, c = (e & 15) * 2;
+          cp_async16(dst + rr * CLD + c, inv + rb * 1024 + rr * 32 + c);
+        }
+      } else {
+        const int hw = min(CW, rb * 32 - q0) / 2;
+        for (int e = tid; e < 32 * hw; e += 128) {
+          const int rr = e / hw, c = (e % hw) * 2;
+          cp_async16(dst + rr * CLD + c, L + (int64_t)(rb * 32 + rr) * nb + q0 + c);
+        }
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
 #pragma unroll
-    for (int u = 0; u < 4; ++u) Wc[(rb * 32 + r) * WLD + c4 + u] = -o[u];
-    __syncthreads();
+  for (int c = 0; c < NCH - 1; ++c) issue(c);
+
+  for (int e = tid; e < 32 * TW; e += 128) {  // diagonal block: columns of Li_cb
+    const int rr = e / TW, c = e % TW;
+    Wc[(cb * 32 + rr) * TW + c] = inv[cb * 1024 + rr * 32 + cc0 + c];
   }
+  int idx = 0;
+  for (int rb = cb + 1; rb < nblk; ++rb) {
+    // T (32 x 8) = L[rb, cb:rb] W[cb:rb, cols]: warp w owns rows 8w..8w+7
+    double acc[2] = {0.0, 0.0};
+    for (int q0 = cb * 32; q0 < rb * 32; q0 += CW, ++idx) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(NCH - 2));
+      __syncthreads();  // chunk idx landed; the slot of idx-1 is free
+      issue(idx + NCH - 1);
+      const double* ch = ring + (idx % NCH) * 32 * CLD + (warp * 8 + fr) * CLD + fk;
+      const double* wb = Wc + (q0 + fk) * TW + fr;
+      const int w = min(CW, rb * 32 - q0);
+#pragma unroll 4
+      for (int k4 = 0; k4 < w; k4 += 4) dmma_884(acc, ch[k4], wb[k4 * TW]);
+    }
+    Tt[(warp * 8 + fr) * TW + 2 * fk] = acc[0];
+    Tt[(warp * 8 + fr) * TW + 2 * fk + 1] = acc[1];
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NCH - 2));
+    __syncthreads();  // T complete; Li_rb landed
+    issue(idx + NCH - 1);
+    const double* li = ring + (idx % NCH) * 32 * CLD + (warp * 8 + fr) * CLD + fk;
+    ++idx;
+    double o[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k4 = 0; k4 < 32; k4 += 4) dmma_884(o, li[k4], Tt[(k4 + fk) * TW + fr]);
+    Wc[(rb * 32 + warp * 8 + fr) * TW + 2 * fk] = -o[0];
+    Wc[(rb * 32 + warp * 8 + fr) * TW + 2 * fk + 1] = -o[1];
+    __syncthreads();  // W_rb visible; Tt reusable
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
   float* WH = g.winv_hi();
   float* WL = g.winv_lo();
-  for (int e = tid; e < nb * 32; e += 256) {
-    const int R = e >> 5, c = e & 31;
-    const double w = R >= cb * 32 ? Wc[R * WLD + c] : 0.0;
+  for (int e = tid; e < nb * TW; e += 128) {
+    const int R = e / TW, c = e % TW;
+    const double w = R >= cb * 32 ? Wc[R * TW + c] : 0.0;
     const float f = __double2float_rn(w);
     uint32_t h;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
-    const int64_t o = (int64_t)R * nb + cb * 32 + c;
+    const int64_t o = (int64_t)R * nb + c0 + c;
     WH[o] = __uint_as_float(h);
     WL[o] = f - __uint_as_float(h);
   }
@@ -315,11 +376,11 @@ __global__ void __launch_bounds__(256) presplit_kernel(Grid g, int k, int64_t s0
 }  // namespace
 
 int mt_trinv_impl(const Grid& g, int k, cudaStream_t st) {
-  const size_t smem = ((size_t)g.nb * WLD + 32 * WLD) * sizeof(double);
+  const size_t smem = ((size_t)g.nb * TW + 32 * TW + (size_t)NCH * 32 * CLD) * sizeof(double);
   cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const double nb = g.nb;
   ProfScope ps(MT_K_MISC, st, nb * nb * nb / 3.0, nb * nb * 16.0);
-  trinv_kernel<<<g.nb / 32, 256, smem, st>>>(g, k);
+  trinv_kernel<<<g.nb / TW, 128, smem, st>>>(g, k);
   MT_LAUNCH_CHECK("trinv_kernel");
   return MT_OK;
 }
