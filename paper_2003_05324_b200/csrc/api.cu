@@ -13,8 +13,11 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <functional>
 #include <mutex>
 #include <vector>
+
+#include <cuda.h>
 
 #include "mt_grid.cuh"
 
@@ -26,7 +29,8 @@ int mt_scan_duplicates_impl(const Grid& g, const double* locs, int metric, doubl
 int mt_matern_array_impl(const double* r, int64_t m, const mt_matern& th, double* out,
                          cudaStream_t st);
 int mt_potrf_impl(const Grid& g, int k, int narrow, cudaStream_t st);
-int mt_trsm_impl(const Grid& g, int k, cudaStream_t st);
+int mt_trsm_impl(const Grid& g, int k, cudaStream_t st,
+                 const std::function<int()>* before = nullptr);
 int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st);
 int mt_logdet_impl(const Grid& g, double* out, double* work, cudaStream_t st);
 int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_t st);
@@ -79,8 +83,12 @@ static int single_gpu_only(const mt_tiles* g, const char* what) {
 
 // ------------------------------------------------------ per-device context
 namespace {
+typedef CUresult (*WriteValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
 struct DevCtx {
   cudaStream_t panel = nullptr;
+  int* yield = nullptr;            // SM-yield request word of the bulk update
+  WriteValueFn write_value = nullptr;
   std::vector<cudaEvent_t> ev;
   size_t next = 0;
   cudaEvent_t event() {
@@ -106,6 +114,16 @@ DevCtx* dev_ctx() {
     }
     c->ev.resize(16);
     for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && cudaMalloc(&c->yield, 64) == cudaSuccess &&
+        cudaMemset(c->yield, 0, 64) == cudaSuccess) {
+      c->write_value = (WriteValueFn)fn;
+    } else {
+      c->yield = nullptr;
+      cudaGetLastError();
+    }
     g_ctx[dev] = c;
   }
   return g_ctx[dev];
@@ -129,6 +147,19 @@ static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main) {
   DevCtx* ctx = dev_ctx();
   if (!ctx) { mt_set_error("cannot create the panel stream"); return MT_E_CUDA; }
   cudaStream_t pan = ctx->panel;
+  // the bulk update (caller stream) yields SMs to the panel kernels on request
+  Grid gb = g;
+  const int ysms = mt_opt_yield_sms();
+  const bool yield_on = ysms > 0 && ctx->yield && ctx->write_value;
+  if (yield_on) gb.yield = ctx->yield;
+  auto request = [&](unsigned v) -> int {
+    if (!yield_on) return MT_OK;
+    if (ctx->write_value((CUstream)pan, (CUdeviceptr)ctx->yield, v, 0) != CUDA_SUCCESS) {
+      mt_set_error("cuStreamWriteValue32 failed");
+      return MT_E_CUDA;
+    }
+    return MT_OK;
+  };
   cudaEvent_t e = ctx->event();
   CK(cudaEventRecord(e, main), "event record");
   CK(cudaStreamWaitEvent(pan, e, 0), "stream wait");
@@ -138,12 +169,18 @@ static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main) {
     cudaEvent_t ep = ctx->event();
     CK(cudaEventRecord(ep, pan), "event record");   // panel k ready
     CK(cudaStreamWaitEvent(main, ep, 0), "stream wait");
-    // panel stream: column k+1 with panel k, then factor panel k+1
+    // panel stream: column k+1 with panel k, then factor panel k+1; the
+    // panel solves ask the bulk update for SMs (its CTAs exit between items)
     RC(mt_update_impl(g, k, k + 1, k + 2, pan));
+    RC(request(1u));
     RC(mt_potrf_impl(g, k + 1, narrow_k(k + 1), pan));
-    if (k + 2 < p) RC(mt_trsm_impl(g, k + 1, pan));
+    if (k + 2 < p) {
+      const std::function<int()> ask = [&]() { return request((unsigned)ysms); };
+      RC(mt_trsm_impl(g, k + 1, pan, yield_on ? &ask : nullptr));
+      RC(request(0u));
+    }
     // caller stream: the rest of step k's trailing update
-    RC(mt_update_impl(g, k, k + 2, p, main));
+    RC(mt_update_impl(gb, k, k + 2, p, main));
     cudaEvent_t em = ctx->event();
     CK(cudaEventRecord(em, main), "event record");  // step k fully applied
     CK(cudaStreamWaitEvent(pan, em, 0), "stream wait");
@@ -185,12 +222,14 @@ static int g_engine = MT_ENGINE_TF32X3;
 static int g_update_ctas = 0;  // 0 = all SMs
 static int g_legacy_dmma = 0;  // 1 = register-staged DMMA band update (A/B comparisons)
 static int g_pcol_ctas = 64;   // CTAs of the lookahead panel-column FP32 update (0 = all SMs)
+static int g_yield_sms = 32;   // SMs the bulk update yields to the panel TRSM (0 = off)
 static int g_tc_trsm = 1;      // 1 = off-band TRSM as a tcgen05 3xTF32 GEMM against L_kk^{-1}
 int mt_opt_engine() { return g_engine; }
 int mt_opt_update_ctas() { return g_update_ctas; }
 int mt_opt_legacy_dmma() { return g_legacy_dmma; }
 int mt_opt_tc_trsm() { return g_tc_trsm; }
 int mt_opt_pcol_ctas() { return g_pcol_ctas; }
+int mt_opt_yield_sms() { return g_yield_sms; }
 
 extern "C" {
 
@@ -201,7 +240,8 @@ int32_t mt_version(void) { return 11; }
  * option 2: 1 = legacy register-staged DMMA band update;
  * option 3: 1 = off-band TRSM as a tcgen05 GEMM against L_kk^{-1} (default),
  *           0 = SIMT substitution against 32x32 inverses;
- * option 4: CTAs of the lookahead panel-column FP32 update (0 = all SMs). Returns old value. */
+ * option 4: CTAs of the lookahead panel-column FP32 update (0 = all SMs);
+ * option 5: SMs the bulk FP32 update yields to the panel TRSM (0 = off). Returns old value. */
 int32_t mt_set_option(int32_t option, int32_t value) {
   int old = -1;
   if (option == 0) { old = g_engine; g_engine = value; }
@@ -209,6 +249,7 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 2) { old = g_legacy_dmma; g_legacy_dmma = value; }
   else if (option == 3) { old = g_tc_trsm; g_tc_trsm = value; }
   else if (option == 4) { old = g_pcol_ctas; g_pcol_ctas = value; }
+  else if (option == 5) { old = g_yield_sms; g_yield_sms = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

@@ -28,6 +28,9 @@ struct Grid {
   // j = c0, c0 + cs, c0 + 2cs, ... (single GPU: cs = 1, c0 = 0)
   int cs = 1, c0 = 0;
   double* dpanel = nullptr;  // multi-GPU: FP64 band rows of the panels in flight
+  // bulk FP32 update only: SM-yield request word written by the panel stream
+  // (cuStreamWriteValue32); CTAs that consume a request exit between work items
+  int* yield = nullptr;
 
   MT_HD int64_t tile_elems() const { return (int64_t)nb * nb; }
   MT_HD bool band(int i, int j) const { return (i - j) < t; }
@@ -178,6 +181,7 @@ int mt_opt_engine();
 int mt_opt_update_ctas();
 int mt_opt_legacy_dmma();
 int mt_opt_pcol_ctas();
+int mt_opt_yield_sms();
 bool mt_dmma_tma_supported(const Grid& g);
 int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st);
 bool mt_tc_supported(const Grid& g);

@@ -148,8 +148,15 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
       for (uint32_t li = 0;; ++li) {
         const int s = li % SCHED;
         mbar_wait(&sempty[s], ((li / SCHED) & 1) ^ 1);
-        int item = atomicAdd(w.counter, 1);
-        if (item >= w.nitems) item = -1;
+        // SM-yield request from the panel stream: this CTA stops taking work
+        // (an oversubscribed grid refills the SM once the panel kernels ran)
+        int item;
+        if (!TRSM && g.yield && *(volatile int*)g.yield > 0 && atomicSub(g.yield, 1) > 0) {
+          item = -1;
+        } else {
+          item = atomicAdd(w.counter, 1);
+          if (item >= w.nitems) item = -1;
+        }
         sitem[s] = item;
         mbar_arrive(&sfull[s]);  // release: consumers see sitem[s]
         if (item < 0) break;
@@ -390,6 +397,7 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
   if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, sizeof(int), st), "counter reset"))
     return MT_E_CUDA;
   int grid = ctas > 0 ? ctas : g_sm_count;
+  if (!trsm && g.yield && ctas <= 0) grid = 2 * g_sm_count;  // room to refill yielded SMs
   if (grid > w.nitems) grid = w.nitems;
   const size_t smem = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   if (trsm) {

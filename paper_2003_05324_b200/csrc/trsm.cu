@@ -18,6 +18,8 @@
 //          inverse published by POTRF -- no sequential substitution)
 // The 32x32 blocks of L and the inverses are streamed through a 4-stage
 // cp.async ring that runs ahead across column blocks.
+#include <functional>
+
 #include "mt_grid.cuh"
 
 #define RC_(call) \
@@ -396,18 +398,22 @@ int mt_presplit_impl(const Grid& g, int k, cudaStream_t st) {
 
 // Panel rows i in (k, p) of tile column k.  Band rows: band slots
 // bcol(k)+1 .. bcol(k+1)-1; off-band rows: off slots scol(k) .. scol(k+1)-1.
-int mt_trsm_impl(const Grid& g, int k, cudaStream_t st) {
+int mt_trsm_impl(const Grid& g, int k, cudaStream_t st, const std::function<int()>* before) {
+  auto pre = [&]() { return before ? (*before)() : MT_OK; };
   if (trsm_smem<double, 32>(g.nb) > 220 * 1024 || trsm_smem<float, 64>(g.nb) > 220 * 1024) {
     mt_set_error("trsm: nb=%d too large for the shared-memory panel", g.nb);
     return MT_E_BAD_ARG;
   }
+  RC_(pre());
   int rc = launch_trsm<double, 32>(g, k, g.bcol(k) + 1, g.bcol(k + 1) - g.bcol(k) - 1, 1, st);
   if (rc) return rc;
   if (g.mode == MT_MODE_MP && g.scol(k + 1) > g.scol(k)) {
     if (mt_tc_trsm_enabled(g)) {
       // the update epilogue of step k-1 pre-split column k (k = 0: nobody did)
       if (k == 0) RC_(mt_presplit_impl(g, k, st));
+      RC_(pre());
       RC_(mt_trinv_impl(g, k, st));
+      RC_(pre());
       rc = mt_tc_trsm_impl(g, k, st);
     } else {
       rc = launch_trsm<float, 64>(g, k, g.scol(k), g.scol(k + 1) - g.scol(k), 0, st);

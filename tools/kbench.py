@@ -11,13 +11,15 @@ ap.add_argument("--n", type=int, default=65536); ap.add_argument("--nb", type=in
 ap.add_argument("--t", type=int, default=2); ap.add_argument("--dp", action="store_true")
 ap.add_argument("--lookahead", type=int, default=0); ap.add_argument("--engine", default="tf32x3")
 ap.add_argument("--legacy-dmma", type=int, default=0); ap.add_argument("--tc-trsm", type=int, default=1)
-ap.add_argument("--pcol", type=int, default=-1)
+ap.add_argument("--pcol", type=int, default=-1); ap.add_argument("--yield-sms", type=int, default=-1)
 a = ap.parse_args()
 mt.set_fp32_engine(a.engine)
 mt.set_legacy_dmma(a.legacy_dmma)
 mt.set_tc_trsm(a.tc_trsm)
 if a.pcol >= 0:
     _lib.load().mt_set_option(4, a.pcol)
+if a.yield_sms >= 0:
+    _lib.load().mt_set_option(5, a.yield_sms)
 KINDS = ["gen64", "gen32", "potrf", "trsm64", "trsm32", "upd64", "upd32", "solve", "misc", "upd64p", "upd32p"]
 locs = mt.generate_locations(a.n, seed=1)
 ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(a.n)))
@@ -38,7 +40,7 @@ for rep in range(2):
     K = len(KINDS); arr = [(ctypes.c_double * K)() for _ in range(3)]; cnt = (ctypes.c_int64 * K)()
     lib.mt_prof_end(K, arr[0], arr[1], arr[2], cnt)
 tot = e0.elapsed_time(e1)
-print(f"n={a.n} nb={a.nb} {pol.label()} la={a.lookahead} legacy_dmma={a.legacy_dmma} tc_trsm={a.tc_trsm} pcol={a.pcol} cholesky {tot:.1f} ms = {a.n**3/3/tot/1e9:.1f} TF/s  status={m.read_status()}")
+print(f"n={a.n} nb={a.nb} {pol.label()} la={a.lookahead} legacy_dmma={a.legacy_dmma} tc_trsm={a.tc_trsm} pcol={a.pcol} yield={a.yield_sms} cholesky {tot:.1f} ms = {a.n**3/3/tot/1e9:.1f} TF/s  status={m.read_status()}")
 for q in range(K):
     if cnt[q]:
         print(f"  {KINDS[q]:7s} launches={cnt[q]:5d} total={arr[0][q]:9.2f} ms avg={arr[0][q]/cnt[q]*1e3:9.1f} us  "
