@@ -462,7 +462,11 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # high-priority NCCL streams: the panel broadcasts get SMs ahead of the
+        # bulk update's pending CTAs (which also yield on request)
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), pg_options=opts)
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist

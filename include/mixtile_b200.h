@@ -165,6 +165,15 @@ int mt_panel(const mt_tiles* g, int32_t k, void* stream);
 /* Step-k trailing updates of the owned columns in [jlo, jhi) (factor.py:266-274);
  * panel k must be present in split/dpanel. */
 int mt_update(const mt_tiles* g, int32_t k, int32_t jlo, int32_t jhi, void* stream);
+/* mt_update with flags: bit 0 = this (bulk) update may yield SMs between work
+ * items when mt_yield_request() posts a request (the caller's panel stream
+ * then gets them for POTRF/TRSM and the broadcast). */
+int mt_update_ex(const mt_tiles* g, int32_t k, int32_t jlo, int32_t jhi, int32_t flags,
+                 void* stream);
+/* Post (in `stream` order, no SM needed: cuStreamWriteValue32) a request that
+ * running yield-enabled bulk updates release `sms` SMs; 0 withdraws it.
+ * No-op when stream memory operations are unavailable. */
+int mt_yield_request(int32_t sms, void* stream);
 /* partial[k] = sum log diag(L_kk) for owned k, 0 otherwise (factor.py:318-323). */
 int mt_logdet_partials(const mt_tiles* g, double* partial, void* stream);
 /* Forward-sweep step i on the owner of column i: y_i = L_ii^{-1} x_i, x_r -= L_ri y_i. */

@@ -85,6 +85,8 @@ SIGNATURES = {
     "mt_set_option": (_I32, [_I32, _I32]),
     "mt_panel": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
     "mt_update": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V]),
+    "mt_update_ex": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _I32, _V]),
+    "mt_yield_request": (ctypes.c_int, [_I32, _V]),
     "mt_logdet_partials": (ctypes.c_int, [_P(MtTiles), _V, _V]),
     "mt_fwd_step": (ctypes.c_int, [_P(MtTiles), _I32, _V, _V]),
     "mt_sumsq": (ctypes.c_int, [_V, _I64, _V, _V, _V]),

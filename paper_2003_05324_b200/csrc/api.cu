@@ -364,6 +364,32 @@ int mt_update(const mt_tiles* t, int32_t k, int32_t jlo, int32_t jhi, void* stre
   return mt_update_impl(g, k, jlo, jhi, (cudaStream_t)stream);
 }
 
+int mt_update_ex(const mt_tiles* t, int32_t k, int32_t jlo, int32_t jhi, int32_t flags,
+                 void* stream) {
+  RC(check_layout(t));
+  Grid g = make_grid(t);
+  if (k < 0 || k >= g.p || jlo <= k || jhi > g.p) {
+    mt_set_error("mt_update_ex: bad step/column range");
+    return MT_E_BAD_ARG;
+  }
+  if (flags & 1) {
+    DevCtx* ctx = dev_ctx();
+    if (ctx && ctx->yield && ctx->write_value) g.yield = ctx->yield;
+  }
+  return mt_update_impl(g, k, jlo, jhi, (cudaStream_t)stream);
+}
+
+int mt_yield_request(int32_t sms, void* stream) {
+  DevCtx* ctx = dev_ctx();
+  if (!ctx || !ctx->yield || !ctx->write_value) return MT_OK;
+  if (ctx->write_value((CUstream)stream, (CUdeviceptr)ctx->yield, (cuuint32_t)(sms > 0 ? sms : 0),
+                       0) != CUDA_SUCCESS) {
+    mt_set_error("cuStreamWriteValue32 failed");
+    return MT_E_CUDA;
+  }
+  return MT_OK;
+}
+
 int mt_logdet_partials(const mt_tiles* t, double* partial, void* stream) {
   RC(check_layout(t));
   return mt_logdet_partials_impl(make_grid(t), partial, (cudaStream_t)stream);

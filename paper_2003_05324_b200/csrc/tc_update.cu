@@ -64,7 +64,7 @@ struct Work {
   int64_t slot0;
   int nitems;  // slots * nsub
   int nsubm, nsubn;
-  int* counter;  // dynamic work queue head (zeroed before the launch)
+  int* counter;  // [dynamic work queue head, CTAs started] (zeroed before the launch)
   int presplit;  // update: also write the pre-TRSM split of column k+1 outputs
 };
 
@@ -144,14 +144,18 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
   if (warp == 0) {
     // ------------------------------------------------ TMA producer + work queue
     if (lane == 0) {
+      if (!TRSM && g.yield) atomicAdd(w.counter + 1, 1);  // CTAs started
       uint32_t it = 0;
       for (uint32_t li = 0;; ++li) {
         const int s = li % SCHED;
         mbar_wait(&sempty[s], ((li / SCHED) & 1) ^ 1);
         // SM-yield request from the panel stream: this CTA stops taking work
         // (an oversubscribed grid refills the SM once the panel kernels ran)
+        // A CTA may only yield while some CTA of the grid has not started yet:
+        // that one is guaranteed to run later and drain the queue.
         int item;
-        if (!TRSM && g.yield && *(volatile int*)g.yield > 0 && atomicSub(g.yield, 1) > 0) {
+        if (!TRSM && g.yield && *(volatile int*)g.yield > 0 &&
+            *(volatile int*)(w.counter + 1) < (int)gridDim.x && atomicSub(g.yield, 1) > 0) {
           item = -1;
         } else {
           item = atomicAdd(w.counter, 1);
@@ -391,10 +395,11 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
   static int* counters[64] = {nullptr};
   static unsigned next_counter[64] = {0};
   if (dev < 0 || dev >= 64) { mt_set_error("device index out of range"); return MT_E_CUDA; }
-  if (!counters[dev] && mt_cuda_check(cudaMalloc(&counters[dev], 256 * sizeof(int)), "counter alloc"))
+  // per launch: [queue head, CTAs started]
+  if (!counters[dev] && mt_cuda_check(cudaMalloc(&counters[dev], 2 * 256 * sizeof(int)), "counter alloc"))
     return MT_E_CUDA;
-  w.counter = counters[dev] + (next_counter[dev]++ % 256);
-  if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, sizeof(int), st), "counter reset"))
+  w.counter = counters[dev] + 2 * (next_counter[dev]++ % 256);
+  if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int), st), "counter reset"))
     return MT_E_CUDA;
   int grid = ctas > 0 ? ctas : g_sm_count;
   if (!trsm && g.yield && ctas <= 0) grid = 2 * g_sm_count;  // room to refill yielded SMs

@@ -3,11 +3,13 @@
 Layout: tile-column-cyclic (the 1 x g case of 2D block-cyclic): rank r stores
 tile columns j = r, r + g, r + 2g, ... in local pools (storage scales as 1/g,
 so full-DP N = 262144 fits on >= 2 B200s).  Step k of the right-looking
-factorization (factor.py:44-80) becomes, with lookahead 1:
+factorization (factor.py:44-80) becomes, with lookahead 1 on two streams:
 
-    owner(k+1):  update(k -> column k+1), POTRF(k+1), TRSM(k+1)
-    everyone:    broadcast panel k+1 from owner(k+1)   (async, NCCL stream)
-    everyone:    update(k -> owned columns k+2 .. p-1)  (overlaps the broadcast)
+    owner(k+1), panel stream:  update(k -> column k+1), POTRF(k+1), TRSM(k+1)
+    everyone, panel stream:    broadcast panel k+1 from owner(k+1) (NCCL)
+    everyone, caller stream:   update(k -> owned columns k+2 .. p-1), which
+                               overlaps the panel chain and the broadcast and
+                               yields SMs to the panel kernels on request
 
 A panel is broadcast as the TF32 hi/lo split of its FP32 operands (rows
 k+1..p-1, what the tcgen05 update reads) plus its FP64 band rows (what the
@@ -36,7 +38,9 @@ def owner(j, world):
 
 
 def schedule(p):
-    """Rank-independent action list of the distributed factorization.
+    """Rank-independent action order of the distributed factorization (what
+    DistributedEvaluator.factor issues, the first three of each step on the
+    panel stream, the last on the caller stream).
 
     ("panel", k)            POTRF(k) + TRSM(k), executed by owner(k)
     ("bcast", k)            panel k broadcast from owner(k) to every rank
@@ -87,6 +91,8 @@ class DistributedEvaluator:
         self.work = torch.empty(2048, dtype=torch.float64, device=dev)
         self.out = torch.empty(1, dtype=torch.float64, device=dev)
         self.flag = torch.empty(3, dtype=torch.int64, device=dev)
+        self.pan = torch.cuda.Stream(device=dev, priority=-1)
+        self.yield_sms = 32  # SMs the bulk update releases to the owner's panel kernels
 
     # -- pieces -------------------------------------------------------------
     def _bcast(self, k, async_op):
@@ -95,21 +101,56 @@ class DistributedEvaluator:
                 for v in panel_slices(self.matrix, k)]
 
     def factor(self):
-        m, lib, st = self.matrix, _lib.load(), _lib.stream_handle()
-        pending = {}
-        for act in schedule(m.p):
-            if act[0] == "panel":
-                k = act[1]
-                if owner(k, self.world) == self.rank:
-                    _lib.check(lib.mt_panel(ctypes.byref(m.desc), k, st), "mt_panel")
-            elif act[0] == "bcast":
-                if self.world > 1:
-                    pending[act[1]] = self._bcast(act[1], async_op=True)
-            else:
-                _, k, jlo, jhi = act
-                for h in pending.pop(k, []):
-                    h.wait()  # the compute stream waits for panel k (non-blocking on host)
-                _lib.check(lib.mt_update(ctypes.byref(m.desc), k, jlo, jhi, st), "mt_update")
+        """The step loop with lookahead 1 on two streams (the single-GPU
+        schedule of csrc/api.cu, with the broadcast in the panel chain):
+
+          panel stream (high priority): update(k -> column k+1) on its owner,
+                         POTRF+TRSM(k+1) on its owner, broadcast of panel k+1
+          caller stream: update(k -> owned columns k+2 ..), which yields SMs
+                         to the owner's panel kernels on request
+
+        The panel stream waits for the caller's step k-1 before touching the
+        panel ring slot of k+1 (= slot of k-1) and column k+1."""
+        torch = _lib.require_cuda()
+        m, lib = self.matrix, _lib.load()
+        d = ctypes.byref(m.desc)
+        main, pan = torch.cuda.current_stream(), self.pan
+        hm, hp = ctypes.c_void_p(main.cuda_stream), ctypes.c_void_p(pan.cuda_stream)
+        mine = lambda k: owner(k, self.world) == self.rank  # noqa: E731
+        bc = {}
+
+        def panel(k):  # on the panel stream
+            if mine(k):
+                _lib.check(lib.mt_yield_request(self.yield_sms, hp), "mt_yield_request")
+                _lib.check(lib.mt_panel(d, k, hp), "mt_panel")
+                _lib.check(lib.mt_yield_request(0, hp), "mt_yield_request")
+            if self.world > 1:
+                with torch.cuda.stream(pan):
+                    bc[k] = self._bcast(k, async_op=True)
+
+        def received(k):  # the current stream waits for panel k's broadcast
+            for h in bc.get(k, []):
+                h.wait()
+
+        pan.wait_stream(main)  # generation of the local tiles
+        panel(0)
+        step_done = None
+        for k in range(m.p - 1):
+            with torch.cuda.stream(pan):
+                if step_done is not None:
+                    pan.wait_event(step_done)  # step k-1 applied everywhere on this rank
+                if mine(k + 1):
+                    received(k)
+                    _lib.check(lib.mt_update(d, k, k + 1, k + 2, hp), "mt_update")
+            panel(k + 1)
+            received(k)
+            bc.pop(k, None)
+            if k + 2 < m.p:
+                _lib.check(lib.mt_update_ex(d, k, k + 2, m.p, 1, hm), "mt_update_ex")
+            step_done = main.record_event()
+        main.wait_stream(pan)
+        received(m.p - 1)
+        bc.clear()
         m._touch()
         m.factored = True
 

@@ -161,3 +161,28 @@ def test_tc_trsm_loglik_parity_strong_field(engine):
         finally:
             mt.set_tc_trsm(old)
         assert abs(ev.value - ref) / abs(ref) < 2e-4, (flag, ev.value, ref)
+
+
+@pytest.mark.parametrize("ysms", [1, 32, 200])
+def test_sm_yield_keeps_results_bitwise(gpu, ysms):
+    """The bulk update's SM-yield protocol only changes which CTA runs which
+    work item: factors equal the no-yield run bit for bit, including small
+    launches where every running CTA could be asked to yield."""
+    mt = _mt()
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    n, nb, t = 4096, 256, 2
+    locs = mt.generate_locations(n, seed=9)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    pol = mt.PrecisionPolicy.mp(diag_thick=t)
+    facs = []
+    for y in (0, ysms):
+        old = lib.mt_set_option(5, y)
+        try:
+            facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), nb,
+                                                           pol), lookahead=1))
+        finally:
+            lib.mt_set_option(5, old)
+    for key in facs[0].tiles:
+        a, b = facs[0].tiles[key], facs[1].tiles[key]
+        assert np.array_equal(a.dp, b.dp), key
