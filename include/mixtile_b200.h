@@ -120,6 +120,17 @@ int mt_scan_duplicates(const mt_tiles* g, const double* locs, int32_t metric, do
 int mt_matern_array(const double* r, int64_t m, const mt_matern* theta, double* out,
                     void* stream);
 
+/* Kriging cross-covariance product (predict.krige, predict.py:37-49: the
+ * `matern_array(pairwise_distance(test, train)) @ weights` step), fused so the
+ * m x n cross-covariance is never stored:
+ *   out[a] = sum_b C(d(test_a, train_b)) w[b],  a < m, b < n,
+ * FP64, fixed reduction order.  test (m x 2), train (n x 2), w (n), out (m):
+ * device; work: mt_cross_work_doubles(m, n) device doubles. */
+int64_t mt_cross_work_doubles(int64_t m, int64_t n);
+int mt_cross_gemv(const double* test, int64_t m, const double* train, int64_t n, int32_t metric,
+                  double radius, const mt_matern* theta, const double* w, double* work,
+                  double* out, void* stream);
+
 /* Band-precision tile Cholesky in place (factor.cholesky, factor.py:230-285):
  * POTRF/TRSM/SYRK/GEMM right-looking with `lookahead` (0 or 1) on a private
  * high-priority panel stream joined back to `stream`.  A non-positive pivot

@@ -72,6 +72,8 @@ SIGNATURES = {
     "mt_generate": (ctypes.c_int, [_P(MtTiles), _V, _I32, _D, _P(MtMatern), _V]),
     "mt_scan_duplicates": (ctypes.c_int, [_P(MtTiles), _V, _I32, _D, _V]),
     "mt_matern_array": (ctypes.c_int, [_V, _I64, _P(MtMatern), _V, _V]),
+    "mt_cross_work_doubles": (_I64, [_I64, _I64]),
+    "mt_cross_gemv": (ctypes.c_int, [_V, _I64, _V, _I64, _I32, _D, _P(MtMatern), _V, _V, _V, _V]),
     "mt_cholesky": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
     "mt_logdet": (ctypes.c_int, [_P(MtTiles), _V, _V, _V]),
     "mt_solve": (ctypes.c_int, [_P(MtTiles), _V, _I64, _I32, _V]),

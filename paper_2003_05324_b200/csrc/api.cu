@@ -39,6 +39,10 @@ int mt_matvec_lower_impl(const Grid& g, const double* v, double* out, cudaStream
 int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st);
 int mt_logdet_partials_impl(const Grid& g, double* partial, cudaStream_t st);
 int mt_sumsq_impl(const double* x, int64_t m, double* work, double* out, cudaStream_t st);
+int64_t mt_cross_work_doubles_impl(int64_t m, int64_t n);
+int mt_cross_gemv_impl(const double* test, int64_t m, const double* train, int64_t n, int metric,
+                       double radius, const mt_matern& th, const double* w, double* work,
+                       double* out, cudaStream_t st);
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[512] = "";
@@ -332,6 +336,20 @@ int mt_matern_array(const double* r, int64_t m, const mt_matern* theta, double* 
                     void* stream) {
   if (!theta || (m > 0 && (!r || !out))) { mt_set_error("null argument"); return MT_E_BAD_ARG; }
   return mt_matern_array_impl(r, m, *theta, out, (cudaStream_t)stream);
+}
+
+int64_t mt_cross_work_doubles(int64_t m, int64_t n) { return mt_cross_work_doubles_impl(m, n); }
+
+int mt_cross_gemv(const double* test, int64_t m, const double* train, int64_t n, int32_t metric,
+                  double radius, const mt_matern* theta, const double* w, double* work,
+                  double* out, void* stream) {
+  if (m < 0 || n < 1 || !theta || (m > 0 && (!test || !train || !w || !work || !out)) ||
+      (metric != MT_METRIC_EUCLIDEAN && metric != MT_METRIC_GREAT_CIRCLE)) {
+    mt_set_error("mt_cross_gemv: bad arguments");
+    return MT_E_BAD_ARG;
+  }
+  return mt_cross_gemv_impl(test, m, train, n, metric, radius, *theta, w, work, out,
+                            (cudaStream_t)stream);
 }
 
 int mt_cholesky(const mt_tiles* t, int32_t lookahead, void* stream) {

@@ -210,7 +210,90 @@ __global__ void matern_array_kernel(const double* __restrict__ r, int64_t m, mt_
     out[e] = mt_matern_value(r[e], th);
 }
 
+// Kriging cross-covariance product (predict.krige, predict.py:37-49):
+//   out[a] = sum_b C(d(test_a, train_b)) w[b]
+// without materialising the m x n cross-covariance.  blockIdx.x covers kTP
+// test points, blockIdx.y one chunk of kChunk training points; each thread
+// reuses a loaded training point for all kTP test points.  Partials are
+// reduced in a fixed order (shuffle tree, then warps in order, then chunks in
+// order), so a test point's value does not depend on m or on its batch.
+constexpr int kTP = 8, kChunk = 4096, kXThreads = 256;
+
+__global__ void __launch_bounds__(kXThreads) cross_partial_kernel(
+    const double2* __restrict__ test, int64_t m, const double2* __restrict__ train, int64_t n,
+    int metric, double radius, mt_matern th, const double* __restrict__ w,
+    double* __restrict__ partial) {
+  const int64_t a0 = (int64_t)blockIdx.x * kTP;
+  const int64_t lo = (int64_t)blockIdx.y * kChunk;
+  const int64_t hi = min(n, lo + kChunk);
+  double2 ta[kTP];
+  double acc[kTP];
+#pragma unroll
+  for (int q = 0; q < kTP; ++q) {
+    ta[q] = a0 + q < m ? test[a0 + q] : make_double2(0.0, 0.0);
+    acc[q] = 0.0;
+  }
+  for (int64_t b = lo + threadIdx.x; b < hi; b += kXThreads) {
+    const double2 pb = train[b];
+    const double wb = w[b];
+#pragma unroll
+    for (int q = 0; q < kTP; ++q) acc[q] += mt_matern_value(dist(ta[q], pb, metric, radius), th) * wb;
+  }
+  __shared__ double red[kXThreads / 32][kTP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < kTP; ++q) {
+    double v = acc[q];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kTP && a0 + threadIdx.x < m) {
+    double s = 0.0;
+    for (int u = 0; u < kXThreads / 32; ++u) s += red[u][threadIdx.x];
+    partial[(int64_t)blockIdx.y * m + a0 + threadIdx.x] = s;
+  }
+}
+
+__global__ void cross_finish_kernel(const double* __restrict__ partial, int64_t m, int nchunks,
+                                    double* __restrict__ out) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < m;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += partial[(int64_t)c * m + a];
+    out[a] = s;
+  }
+}
+
 }  // namespace
+
+int64_t mt_cross_work_doubles_impl(int64_t m, int64_t n) {
+  return ((n + kChunk - 1) / kChunk) * (m > 0 ? m : 1);
+}
+
+int mt_cross_gemv_impl(const double* test, int64_t m, const double* train, int64_t n, int metric,
+                       double radius, const mt_matern& th, const double* w, double* work,
+                       double* out, cudaStream_t st) {
+  if (m <= 0) return MT_OK;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int64_t mblocks = (m + kTP - 1) / kTP;
+  if (nchunks > 65535 || mblocks > (int64_t)INT32_MAX) {
+    mt_set_error("cross-covariance product too large (m=%lld, n=%lld)", (long long)m, (long long)n);
+    return MT_E_BAD_ARG;
+  }
+  {
+    ProfScope ps(MT_K_MISC, st, 0.0, (double)(m + n) * 16.0 + n * 8.0 + m * 8.0);
+    dim3 grid((unsigned)mblocks, (unsigned)nchunks);
+    cross_partial_kernel<<<grid, kXThreads, 0, st>>>((const double2*)test, m, (const double2*)train,
+                                                     n, metric, radius, th, w, work);
+    MT_LAUNCH_CHECK("cross_partial_kernel");
+  }
+  int64_t blocks = (m + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cross_finish_kernel<<<(unsigned)blocks, 256, 0, st>>>(work, m, (int)nchunks, out);
+  MT_LAUNCH_CHECK("cross_finish_kernel");
+  return MT_OK;
+}
 
 int mt_generate_impl(const Grid& g, const double* locs, int metric, double radius,
                      const mt_matern& th, cudaStream_t st) {

@@ -131,3 +131,34 @@ def generate_field(locations, params, metric=None, seed=0, nb=256):
         raise RuntimeError(f"covariance not positive definite: {exc}") from exc
     v = np.random.default_rng(seed).standard_normal(n)
     return GeoDataset(locations, _factor.matvec_lower(fac, v), metric)
+
+
+@dataclass(frozen=True)
+class FoldAssignment:
+    """k-fold partition of n rows (geodata.py:114-121)."""
+
+    k: int
+    fold_of: np.ndarray
+    folds: tuple
+
+    @property
+    def n(self):
+        return self.fold_of.shape[0]
+
+
+def kfold_split(n, k, seed=0):
+    """Random partition into k folds whose sizes differ by at most one: the
+    first n % k folds get one extra row; each fold's rows are sorted
+    (geodata.py:124-146, same generator draws so folds match the reference)."""
+    if n < 1:
+        raise ValueError(f"need n >= 1, got {n}")
+    if k < 2 or k > n:
+        raise ValueError(f"need 2 <= k <= n, got k={k}, n={n}")
+    perm = np.random.default_rng(seed).permutation(n)
+    sizes = [n // k + (1 if f < n % k else 0) for f in range(k)]
+    bounds = np.concatenate(([0], np.cumsum(sizes)))
+    folds = tuple(np.sort(perm[bounds[f]:bounds[f + 1]]) for f in range(k))
+    fold_of = np.empty(n, dtype=np.int64)
+    for f, idx in enumerate(folds):
+        fold_of[idx] = f
+    return FoldAssignment(k=k, fold_of=fold_of, folds=folds)

@@ -152,6 +152,31 @@ def fit_case():
     print("fit", {k: v["params"] for k, v in meta.items()})
 
 
+def krige_case():
+    """predict.krige / pmse_kfold outputs of the reference (predict.py:37-92)."""
+    from mixtile import predict
+    out = {}
+    meta = {}
+    th = covmath.MaternParams(1.4, 0.12, 1.5)
+    ds = _sim(300, 5, th, nb=64, sort=False)
+    test = geodata.generate_locations(37, seed=99)
+    out.update(locs=ds.locations, z=ds.z, test=test, theta=np.array(th.as_tuple()))
+    for tag in ("dp", "mp:1", "mp:2"):
+        out[f"pred_{tag.replace(':', '_')}"] = predict.krige(ds, test, th, 64, _policy(tag))
+    th2 = covmath.MaternParams(1.0, 0.1, 0.5)
+    ds2 = _sim(200, 6, th2, nb=64, sort=False)
+    out.update(locs2=ds2.locations, z2=ds2.z)
+    rep = predict.pmse_kfold(ds2, th2, 32, _policy("mp:1"), k=5, seed=3)
+    out["pmse_pred"] = rep.predictions
+    meta["pmse"] = rep.pmse
+    meta["fold_mse"] = list(rep.fold_mse)
+    folds = geodata.kfold_split(23, 4, seed=7)
+    out["fold_of_23_4_7"] = folds.fold_of
+    out["results"] = np.array(json.dumps(meta))
+    np.savez_compressed(os.path.join(OUT, "krige.npz"), **out)
+    print("krige", meta)
+
+
 def main():
     print("reference mixtile", mixtile.__version__)
     th1 = covmath.MaternParams(1.0, 0.1, 0.5)
@@ -171,6 +196,7 @@ def main():
     assembly_case()
     flops_case()
     fit_case()
+    krige_case()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,95 @@
+"""GPU: kriging (predict.krige / pmse_kfold, predict.py:37-92) vs the reference.
+
+The device path factors the training covariance under the policy, solves on
+the device and forms cross_cov @ weights with the fused mt_cross_gemv kernel.
+Checked against the reference's frozen outputs (tests/golden/krige.npz), the
+oracle at a larger size, and the reference's own test properties
+(test_predict.py): interpolation, far-field prior mean, batch == singletons,
+MP(t=p) == DP bitwise.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import mixtile_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _mt():
+    import paper_2003_05324_b200 as mt
+    return mt
+
+
+@pytest.mark.parametrize("tag", ["dp", "mp_1", "mp_2"])
+def test_krige_matches_reference(gpu, tag):
+    mt = _mt()
+    g = load_golden("krige")
+    ds = mt.GeoDataset(g["locs"], g["z"])
+    pol = mt.PrecisionPolicy.dp() if tag == "dp" else mt.PrecisionPolicy.mp(
+        diag_thick=int(tag.split("_")[1]))
+    pred = mt.krige(ds, g["test"], mt.MaternParams(*g["theta"]), 64, pol)
+    want = g[f"pred_{tag}"]
+    # DP: the reference's own dense-oracle tolerance (test_predict.py:51); MP:
+    # FP32 off-band factor, same band as the reference
+    atol = 1e-9 if tag == "dp" else 1e-5
+    np.testing.assert_allclose(pred, want, rtol=0, atol=atol)
+
+
+def test_pmse_kfold_matches_reference(gpu):
+    mt = _mt()
+    g = load_golden("krige")
+    ds = mt.GeoDataset(g["locs2"], g["z2"])
+    rep = mt.pmse_kfold(ds, mt.MaternParams(1.0, 0.1, 0.5), 32,
+                        mt.PrecisionPolicy.mp(diag_thick=1), k=5, seed=3)
+    np.testing.assert_allclose(rep.predictions, g["pmse_pred"], rtol=0, atol=1e-5)
+    assert abs(rep.pmse - g["results"]["pmse"]) <= 1e-5 * g["results"]["pmse"] + 1e-7
+
+
+def test_krige_vs_oracle_larger(gpu):
+    mt = _mt()
+    n, nb = 2048, 256
+    locs = mt.generate_locations(n, seed=21)
+    z = np.random.default_rng(22).standard_normal(n)
+    test = mt.generate_locations(300, seed=23)
+    th = (1.0, 0.1, 0.5)
+    for mode, t, atol in (("dp", 8, 1e-8), ("mp", 2, 1e-4)):
+        pol = mt.PrecisionPolicy.dp() if mode == "dp" else mt.PrecisionPolicy.mp(diag_thick=t)
+        got = mt.krige(mt.GeoDataset(locs, z), test, mt.MaternParams(*th), nb, pol)
+        want = O.krige(locs, z, test, th, nb, mode, t)
+        scale = np.max(np.abs(want))
+        assert np.max(np.abs(got - want)) <= atol * scale, (mode, np.max(np.abs(got - want)))
+
+
+def test_krige_properties(gpu):
+    mt = _mt()
+    th = mt.MaternParams(1.0, 0.1, 0.5)
+    ds = mt.generate_field(mt.generate_locations(40, seed=1), th, seed=2)
+    dp = mt.PrecisionPolicy.dp()
+    # interpolates training points (test_predict.py:22-25)
+    np.testing.assert_allclose(mt.krige(ds, ds.locations, th, 8, dp), ds.z, rtol=0, atol=1e-6)
+    # far field -> prior mean 0 (test_predict.py:28-32)
+    assert abs(mt.krige(ds, np.array([[50.0, 50.0]]), th, 8, dp)[0]) < 1e-8
+    # batch == singletons (fixed-order reduction: bitwise, stronger than the reference's 1e-12)
+    test = mt.generate_locations(6, seed=44)
+    batch = mt.krige(ds, test, th, 8, dp)
+    singles = np.array([mt.krige(ds, test[i:i + 1], th, 8, dp)[0] for i in range(6)])
+    assert np.array_equal(batch, singles)
+    # MP with the band covering everything == DP bitwise (test_predict.py:62-66)
+    a = mt.krige(ds, test, th, 8, dp)
+    b = mt.krige(ds, test, th, 8, mt.PrecisionPolicy.mp(diag_thick=5))
+    assert np.array_equal(a, b)
+    c = mt.krige(ds, test, th, 8, mt.PrecisionPolicy.mp(diag_thick=1))
+    assert not np.array_equal(a, c) and np.allclose(a, c, rtol=0, atol=1e-4)
+    # general nu (Bessel path) and great-circle distances
+    th2 = mt.MaternParams(1.2, 300.0, 0.8)
+    gc = mt.DistanceMetric.great_circle()
+    rng = np.random.default_rng(5)
+    ll = np.column_stack([rng.uniform(-30, 30, 50), rng.uniform(-20, 20, 50)])
+    dsg = mt.GeoDataset(ll, rng.standard_normal(50), gc)
+    tl = np.column_stack([rng.uniform(-30, 30, 7), rng.uniform(-20, 20, 7)])
+    got = mt.krige(dsg, tl, th2, 16, dp)
+    want = O.krige(ll, dsg.z, tl, th2.as_tuple(), 16, "dp", 4, metric="great_circle",
+                   radius=gc.radius)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-9)
