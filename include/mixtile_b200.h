@@ -241,7 +241,16 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   2: 1 = register-staged DMMA band update instead of the TMA-staged one
  *   3: off-band panel TRSM: 1 = tcgen05 3xTF32 GEMM against L_kk^{-1} (default),
  *      0 = SIMT blocked substitution against 32x32 diagonal-block inverses
- *   4: CTAs of the lookahead panel-column FP32 update (0 = all SMs) */
+ *   4: CTAs of the lookahead panel-column FP32 update (0 = all SMs)
+ *   5: SMs the bulk FP32 update yields to the panel kernels on request (0 = off)
+ *   6: super-column width (owned tile columns) of the bulk FP32 update's output
+ *      order, for L2 reuse of the panel operands (0 = column-by-column slot order)
+ *   7: 1 = the FP32 update prefetches each work item's C block into L2 when the
+ *      item is dequeued (cp.async.bulk.prefetch.L2), 0 = off
+ *   8: diagnostics of the FP32 update epilogue (timing only, WRONG results):
+ *      bit 0 skip C loads, bit 1 skip C stores, bit 2 skip the epilogue
+ *   9: 1 = FP32 update and off-band TRSM on CTA pairs (tcgen05.mma.cta_group::2,
+ *      M = 256, each CTA stages half of B; default), 0 = single-CTA kernel */
 int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */

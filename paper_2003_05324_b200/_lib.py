@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmixtile_b200.so")
+# MIXTILE_LIB: load a differently-built copy (A/B of compile-time kernel variants)
+LIB_PATH = os.environ.get("MIXTILE_LIB") or os.path.join(HERE, "libmixtile_b200.so")
 
 MT_OK, MT_E_NOT_SPD, MT_E_OVERFLOW, MT_E_BAD_ARG, MT_E_CUDA = 0, 1, 2, 3, 4
 MODE_CODE = {"dp": 0, "mp": 1, "dst": 2}

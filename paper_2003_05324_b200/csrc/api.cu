@@ -228,12 +228,20 @@ static int g_legacy_dmma = 0;  // 1 = register-staged DMMA band update (A/B comp
 static int g_pcol_ctas = 64;   // CTAs of the lookahead panel-column FP32 update (0 = all SMs)
 static int g_yield_sms = 32;   // SMs the bulk update yields to the panel TRSM (0 = off)
 static int g_tc_trsm = 1;      // 1 = off-band TRSM as a tcgen05 3xTF32 GEMM against L_kk^{-1}
+static int g_super_cols = 0;   // super-column width of the bulk FP32 update order (0 = slot order)
+static int g_cta_pairs = 1;    // 1 = FP32 update/TRSM on CTA pairs (tcgen05 cta_group::2)
+static int g_tc_diag = 0;      // diagnostics (wrong results): 1 no C loads, 2 no C stores, 4 no epilogue
+static int g_c_prefetch = 0;   // 1 = FP32 update stages each item's C block in L2 (cp.async.bulk.prefetch)
 int mt_opt_engine() { return g_engine; }
 int mt_opt_update_ctas() { return g_update_ctas; }
 int mt_opt_legacy_dmma() { return g_legacy_dmma; }
 int mt_opt_tc_trsm() { return g_tc_trsm; }
 int mt_opt_pcol_ctas() { return g_pcol_ctas; }
 int mt_opt_yield_sms() { return g_yield_sms; }
+int mt_opt_super_cols() { return g_super_cols; }
+int mt_opt_c_prefetch() { return g_c_prefetch; }
+int mt_opt_tc_diag() { return g_tc_diag; }
+int mt_opt_cta_pairs() { return g_cta_pairs; }
 
 extern "C" {
 
@@ -245,7 +253,14 @@ int32_t mt_version(void) { return 11; }
  * option 3: 1 = off-band TRSM as a tcgen05 GEMM against L_kk^{-1} (default),
  *           0 = SIMT substitution against 32x32 inverses;
  * option 4: CTAs of the lookahead panel-column FP32 update (0 = all SMs);
- * option 5: SMs the bulk FP32 update yields to the panel TRSM (0 = off). Returns old value. */
+ * option 5: SMs the bulk FP32 update yields to the panel TRSM (0 = off);
+ * option 6: super-column width of the FP32 update's output order (0 = slot order);
+ * option 7: 1 = the FP32 update prefetches each work item's C block into L2;
+ * option 8: diagnostics of the FP32 update epilogue (WRONG RESULTS, timing only):
+ *           bit 0 skip C loads, bit 1 skip C stores, bit 2 skip the epilogue;
+ * option 9: 1 = FP32 update / off-band TRSM on CTA pairs (tcgen05.mma.cta_group::2,
+ *           default), 0 = single-CTA kernel.
+ * Returns the old value. */
 int32_t mt_set_option(int32_t option, int32_t value) {
   int old = -1;
   if (option == 0) { old = g_engine; g_engine = value; }
@@ -254,6 +269,10 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 3) { old = g_tc_trsm; g_tc_trsm = value; }
   else if (option == 4) { old = g_pcol_ctas; g_pcol_ctas = value; }
   else if (option == 5) { old = g_yield_sms; g_yield_sms = value; }
+  else if (option == 6) { old = g_super_cols; g_super_cols = value; }
+  else if (option == 7) { old = g_c_prefetch; g_c_prefetch = value; }
+  else if (option == 8) { old = g_tc_diag; g_tc_diag = value; }
+  else if (option == 9) { old = g_cta_pairs; g_cta_pairs = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

@@ -188,4 +188,10 @@ bool mt_tc_supported(const Grid& g);
 bool mt_tc_trsm_enabled(const Grid& g);  // off-band TRSM as a tcgen05 GEMM against L_kk^{-1}
 int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st);
 int mt_opt_tc_trsm();
-int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st);
+int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st);
+int mt_opt_super_cols();
+int mt_opt_c_prefetch();
+int mt_opt_tc_diag();
+int mt_opt_cta_pairs();
+int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
+                  int presplit, cudaStream_t st);

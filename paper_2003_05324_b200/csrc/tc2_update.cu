@@ -1,0 +1,442 @@
+// FP32 (off-band) trailing update and off-band panel TRSM on CTA PAIRS:
+// tcgen05.mma.cta_group::2, 3xTF32 (same arithmetic as tc_update.cu).
+//
+//   C_ij <- C_ij - A_ik A_jk^T      (kernels.gemm FP32 path, factor.py:273-274)
+//   X_ik  = B_ik W^T, W = L_kk^-1   (kernels.trsm FP32 path, factor.py:264)
+//
+// Why pairs: the single-CTA kernel (M=128, N=256) stages 48 KB of TF32 hi/lo
+// operands per 16-wide K slab through TMA, i.e. 64 B/clk/SM at full MMA rate,
+// above what L2->SM delivers (~42 B/clk/SM chip-wide, B300_MICROARCH "TMA
+// chip-throughput"); ncu showed the tensor pipe ~68% busy with the MMA issuer
+// waiting on operands.  A CTA pair computes a 256 x 256 block with one
+// M=256 UMMA: each CTA stages its own 128 rows of A and HALF of B (128 rows),
+// 32 KB per slab for the same MMA time -- 1.5x less operand traffic per flop.
+//
+// Roles (192 threads per CTA, one CTA per SM, cluster (2,1,1)):
+//   warp 0  TMA producer in both CTAs; the leader (rank 0) also owns the
+//           dynamic work queue and forwards each item to the peer through
+//           distributed shared memory.  Both CTAs' TMA loads complete on the
+//           leader's `full` barrier (cta_group::2 TMA).
+//   warp 1  leader: single-thread tcgen05.mma.cta_group::2 issuer; its commits
+//           multicast to both CTAs' `empty` / `tfull` barriers.  Both CTAs'
+//           warp 1 allocate / free TMEM (cta_group::2).
+//   warps 2-5  epilogue of the CTA's own 128 accumulator rows (TMEM lanes),
+//           as in tc_update.cu; they release the accumulator on the leader's
+//           `tempty` (4 local + 4 remote arrivals).
+// Every output element is produced by one pair per step with the same MMA
+// sequence as a function of its position only: deterministic and
+// schedule-invariant (bitwise equal to the single-CTA kernel is NOT claimed:
+// the K-slab order is the same, so it is, but tests check it explicitly).
+#include <cuda.h>
+
+#include "tma.cuh"
+
+namespace {
+using namespace mt_tma;
+
+constexpr int BM = 128;               // accumulator rows per CTA (pair M = 256)
+constexpr int BN = 256;               // pair N; each CTA stages BN / 2 rows of B
+constexpr int BNH = BN / 2;
+constexpr int BK = 16, STAGES = 6;
+constexpr int A_BYTES = BM * BK * 4;  // 8 KB
+constexpr int B_BYTES = BNH * BK * 4; // 8 KB
+constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
+constexpr int NUM_THREADS = 192;
+constexpr int EPI_STRIDE = 33;
+constexpr int EPI_BYTES = 4 * 32 * EPI_STRIDE * 4;
+constexpr int TMEM_COLS = 512;        // 2 accumulators x 256 columns
+constexpr int SCHED = 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
+
+__device__ __forceinline__ uint64_t sw64_desc(const void* p) {
+  const uint64_t a = (smem_u32(p) >> 4) & 0x3FFF;
+  return a | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) | (4ull << 61);
+}
+// kind::tf32, D f32, A/B tf32 K-major, N = 256, M = 256 (cta_group::2)
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank`
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void st_cl_u32(uint32_t cl_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+// TMA into this CTA's smem; completion bytes counted on the LEADER's barrier
+__device__ __forceinline__ void tma_load_pair(void* dst, const CUtensorMap* map, uint32_t bar_cl,
+                                              int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(bar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+// arrive (once) on the barrier at this smem offset in both CTAs when the MMAs finish
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+struct Work2 {
+  int64_t slot0;
+  int nitems;    // slots * nsubm * nsubn (pair items of 256 x 256)
+  int nsubm, nsubn;
+  int* counter;  // [work queue head, pairs started]
+  int presplit;
+};
+
+template <bool TRSM>
+__device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
+                                         const CUtensorMap& map_a, const CUtensorMap& map_b) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* epi = (float*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES + EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + SCHED;
+  int* sitem = (int*)(sempty + SCHED);
+  int* si = sitem + SCHED;  // tile row i of the item
+  int* sj = si + SCHED;     // tile column j of the item
+  uint32_t* tmem_slot = (uint32_t*)(sj + SCHED);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int nb = g.nb;
+  const int nsub = w.nsubm * w.nsubn;
+  auto item_ksteps = [&](int item) {
+    return TRSM ? ((item % nsub) % w.nsubn + 1) * (BN / BK) : nb / BK;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive.expect_tx (both CTAs' bytes)
+      mbar_init(&empty[s], 1);  // one multicast commit per use
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // leader: 4 local + 4 peer epilogue warps
+    }
+    for (int s = 0; s < SCHED; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 10);  // leader: MMA + 4 epi + peer producer + 4 peer epi
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_of = [&](int item, int& i, int& j) {
+    g.off_slot_ij(w.slot0 + item / nsub, i, j);
+  };
+  // consumer side of the work ring (both CTAs); the peer releases the
+  // leader's slot remotely
+  auto next_item = [&](uint32_t li, int* pi, int* pj) {
+    const int s = li % SCHED;
+    mbar_wait_cl(&sfull[s], (li / SCHED) & 1);
+    const int item = *(volatile int*)&sitem[s];
+    if (pi) {
+      *pi = *(volatile int*)&si[s];
+      *pj = *(volatile int*)&sj[s];
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (leader) mbar_arrive(&sempty[s]);
+      else mbar_arrive_cl(peer_addr(&sempty[s], 0));
+    }
+    return item;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ work queue + TMA producer
+    if (lane == 0) {
+      if (leader && !TRSM && g.yield) atomicAdd(w.counter + 1, 1);  // pairs started
+      const int npairs = (int)(gridDim.x / 2);
+      uint32_t it = 0;
+      for (uint32_t li = 0;; ++li) {
+        const int s = li % SCHED;
+        int item, i = 0, j = 0;
+        if (leader) {
+          mbar_wait(&sempty[s], ((li / SCHED) & 1) ^ 1);
+          // the pair stops on a failed pivot or on an SM-yield request (only while
+          // some pair has not started: that one will drain the queue)
+          if (g.failed()) {
+            item = -1;
+          } else if (!TRSM && g.yield && *(volatile int*)g.yield > 0 &&
+                     *(volatile int*)(w.counter + 1) < npairs && atomicSub(g.yield, 2) > 0) {
+            item = -1;
+          } else {
+            item = atomicAdd(w.counter, 1);
+            if (item >= w.nitems) item = -1;
+          }
+          if (item >= 0) tile_of(item, i, j);
+          sitem[s] = item; si[s] = i; sj[s] = j;
+          st_cl_u32(peer_addr(&sitem[s], 1), (uint32_t)item);
+          st_cl_u32(peer_addr(&si[s], 1), (uint32_t)i);
+          st_cl_u32(peer_addr(&sj[s], 1), (uint32_t)j);
+          mbar_arrive(&sfull[s]);
+          mbar_arrive_cl(peer_addr(&sfull[s], 1));  // release: the peer sees the item
+        } else {
+          mbar_wait_cl(&sfull[s], (li / SCHED) & 1);
+          item = *(volatile int*)&sitem[s];
+          i = *(volatile int*)&si[s];
+          j = *(volatile int*)&sj[s];
+          mbar_arrive_cl(peer_addr(&sempty[s], 0));
+        }
+        if (item < 0) break;
+        const int sub = item % nsub;
+        const int m0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM;
+        const int n0 = (sub % w.nsubn) * BN + (int)rank * BNH;
+        // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb;
+        // TRSM: A = pre-split of B_ik, B = split of W = L_kk^{-1}
+        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
+        const int brow = TRSM ? (int)g.winv_row() + n0 : ((k & 1) * g.p + j) * 2 * nb + n0;
+        const int ksteps = item_ksteps(item);
+        for (int ks = 0; ks < ksteps; ++ks, ++it) {
+          const int st = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[st], ph ^ 1);
+          unsigned char* sb = smem + st * STAGE_BYTES;
+          if (leader) mbar_expect_tx(&full[st], 2 * STAGE_BYTES);
+          const uint32_t bar = peer_addr(&full[st], 0);
+          tma_load_pair(sb, &map_a, bar, ks * BK, arow);                               // A hi
+          tma_load_pair(sb + A_BYTES, &map_b, bar, ks * BK, brow);                     // B hi
+          tma_load_pair(sb + A_BYTES + B_BYTES, &map_a, bar, ks * BK, arow + nb);      // A lo
+          tma_load_pair(sb + 2 * A_BYTES + B_BYTES, &map_b, bar, ks * BK, brow + nb);  // B lo
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      uint32_t it = 0;
+      for (uint32_t li = 0;; ++li) {
+        const int item = next_item(li, nullptr, nullptr);
+        if (item < 0) break;
+        const int ksteps = item_ksteps(item);
+        const uint32_t b = li & 1, aph = (li >> 1) & 1;
+        mbar_wait_cl(&tempty[b], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t dcol = tmem_base + b * BN;
+        for (int ks = 0; ks < ksteps; ++ks, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            unsigned char* st = smem + s * STAGE_BYTES;
+            const unsigned char* ahi = st;
+            const unsigned char* bhi = st + A_BYTES;
+            const unsigned char* alo = st + A_BYTES + B_BYTES;
+            const unsigned char* blo = alo + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const int off = kk * 32;  // 8 fp32 along K = 32 B inside the 64 B swizzle row
+              const uint32_t first = (ks == 0 && kk == 0) ? 0u : 1u;
+              umma2_tf32(dcol, sw64_desc(alo + off), sw64_desc(bhi + off), first);
+              umma2_tf32(dcol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
+              umma2_tf32(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off), 1u);
+            }
+            umma2_commit_both(&empty[s]);                        // both CTAs' stage s free
+            if (ks == ksteps - 1) umma2_commit_both(&tfull[b]);  // both accumulators ready
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
+    const uint32_t tempty_leader[2] = {peer_addr(&tempty[0], 0), peer_addr(&tempty[1], 0)};
+    for (uint32_t li = 0;; ++li) {
+      int i, j;
+      const int item = next_item(li, &i, &j);
+      if (item < 0) break;
+      const int sub = item % nsub;
+      const int m0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM, n0 = (sub % w.nsubn) * BN;
+      const uint32_t b = li & 1, aph = (li >> 1) & 1;
+      const int64_t roff = (int64_t)(m0 + q * 32) * nb + n0;
+      float* cbase = g.stile(i, j) + roff;
+      float cn[32];
+      if constexpr (!TRSM) {
+#pragma unroll
+        for (int r = 0; r < 32; ++r) cn[r] = cbase[(int64_t)r * nb + lane];
+      }
+      mbar_wait(&tfull[b], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      float* shi = TRSM ? g.split_hi(i, k) + roff
+                        : ((w.presplit && j == k + 1) ? g.presplit_hi(i) + roff : nullptr);
+      const int64_t te = g.tile_elems();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr + c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 32; ++u) stg[lane * EPI_STRIDE + u] = __uint_as_float(v[u]);
+        __syncwarp();
+        float* cp = cbase + c + lane;
+        float cv[32];
+        if constexpr (TRSM) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) cv[r] = stg[r * EPI_STRIDE + lane];
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) cv[r] = cn[r];
+          if (c + 32 < BN) {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) cn[r] = cp[(int64_t)r * nb + 32];
+          }
+#pragma unroll
+          for (int r = 0; r < 32; ++r) cv[r] -= stg[r * EPI_STRIDE + lane];
+        }
+#pragma unroll
+        for (int r = 0; r < 32; ++r) cp[(int64_t)r * nb] = cv[r];
+        if (shi) {
+          float* hrow = shi + c + lane;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            uint32_t h;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(cv[r]));
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(__uint_as_float(h)) : "memory");
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(cv[r] - __uint_as_float(h))
+                         : "memory");
+            asm volatile("" : "+l"(hrow));
+            hrow += nb;
+          }
+        }
+        __syncwarp();
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cl(tempty_leader[b]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();  // no remote arrive / MMA of the pair still targets this CTA
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    tc2_update_kernel(Grid g, int k, Work2 w, const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b) {
+  tc2_body<false>(g, k, w, map_a, map_b);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    tc2_trsm_kernel(Grid g, int k, Work2 w, const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b) {
+  tc2_body<true>(g, k, w, map_a, map_b);
+}
+
+int g_sm2 = 0;
+
+}  // namespace
+
+// launch over the off-band slot range [s0, s0 + scnt) of step k; `ctas` caps
+// the grid (rounded down to pairs)
+int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
+                  int presplit, cudaStream_t st) {
+  if (scnt <= 0) return MT_OK;
+  CUtensorMap ma, mb;
+  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
+  int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  Work2 w;
+  w.slot0 = s0;
+  w.nsubm = g.nb / (2 * BM);
+  w.nsubn = g.nb / BN;
+  w.nitems = (int)(scnt * w.nsubm * w.nsubn);
+  w.presplit = presplit;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_sm2) cudaDeviceGetAttribute(&g_sm2, cudaDevAttrMultiProcessorCount, dev);
+  static int* counters[64] = {nullptr};
+  static unsigned next_counter[64] = {0};
+  if (dev < 0 || dev >= 64) { mt_set_error("device index out of range"); return MT_E_CUDA; }
+  if (!counters[dev] && mt_cuda_check(cudaMalloc(&counters[dev], 2 * 256 * sizeof(int)), "counter alloc"))
+    return MT_E_CUDA;
+  w.counter = counters[dev] + 2 * (next_counter[dev]++ % 256);
+  if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int), st), "counter reset"))
+    return MT_E_CUDA;
+  int pairs = (ctas > 0 ? ctas : g_sm2) / 2;
+  if (!trsm && g.yield && ctas <= 0) pairs = g_sm2;  // oversubscribed: refills yielded SMs
+  if (pairs > w.nitems) pairs = w.nitems;
+  if (pairs < 1) pairs = 1;
+  const size_t smem = SMEM_BYTES;
+  if (trsm) {
+    cudaFuncSetAttribute(tc2_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tc2_trsm_kernel<<<2 * pairs, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+    MT_LAUNCH_CHECK("tc2_trsm_kernel");
+  } else {
+    cudaFuncSetAttribute(tc2_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tc2_update_kernel<<<2 * pairs, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+    MT_LAUNCH_CHECK("tc2_update_kernel");
+  }
+  return MT_OK;
+}

@@ -34,9 +34,16 @@ constexpr int BM = 128, BN = 256, BK = 16, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 4;          // 8 KB
 constexpr int B_BYTES = BN * BK * 4;          // 16 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 48 KB
-constexpr int NUM_THREADS = 192;
-constexpr int EPI_STRIDE = 33;                        // transpose tile, conflict-free
-constexpr int EPI_BYTES = 4 * 32 * EPI_STRIDE * 4;    // 4 warps x 32x33 floats
+#ifndef MT_EPI_WARPS
+#define MT_EPI_WARPS 4
+#endif
+// epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
+// taking half of the item's columns: twice the C loads in flight)
+constexpr int EPI_WARPS = MT_EPI_WARPS;
+constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI_STRIDE = 33;                                // transpose tile, conflict-free
+constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_STRIDE * 4;    // per warp 32x33 floats
 constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 columns
 
 // K-major, SWIZZLE_64B smem matrix descriptor (8-row atoms of 64 B, SBO = 512 B)
@@ -66,7 +73,60 @@ struct Work {
   int nsubm, nsubn;
   int* counter;  // [dynamic work queue head, CTAs started] (zeroed before the launch)
   int presplit;  // update: also write the pre-TRSM split of column k+1 outputs
+  int mlo, mhi;  // update: owned tile-column index range [mlo, mhi) of the outputs
+  int sw;        // update: super-column width (owned columns); 0 = slot order
+  int l2pf;      // update: prefetch each item's C block into L2 when it is dequeued
+  int diag;      // diagnostics only (option 8): 1 skip C loads, 2 skip C stores, 4 skip epilogue
 };
+
+// ---- L2-friendly output order of the trailing update -----------------------
+// Slot order (column by column) re-reads every row operand A_ik from HBM once
+// per output column: at p - k = 500 the panel split (2 MB per tile) is far
+// larger than L2.  Instead the outputs are visited in super-columns of `sw`
+// owned columns, rows ascending inside each, columns ascending inside a row:
+// a row operand is then fetched once per super-column and the sw column
+// operands stay L2-resident while the rows sweep past.  Every output tile is
+// still computed by exactly one work item, so results do not depend on it.
+//
+// Owned column m is global column j = c0 + m*cs; its off-band rows are
+// i in [j + t, p).  In a super-column [ma, mb) row i holds the columns
+// m in [ma, min(mb, F(i) + 1)), F(i) = floor((i - t - c0) / cs), so the tiles
+// before row x number P(x) = G(x, ma) - G(x, mb) with
+// G(x, a) = sum_{i<x} max(0, floor((i - d_a) / cs)), d_a = t + c0 + (a - 1) cs,
+// = T(x - d_a) - T(-d_a),  T(Y) = sum_{y<Y} floor(y / cs)  (0 for Y <= 0).
+__device__ __forceinline__ int64_t stair_T(int64_t y, int cs) {
+  if (y <= 0) return 0;
+  const int64_t q = y / cs, r = y % cs;
+  return (int64_t)cs * q * (q - 1) / 2 + r * q;
+}
+__device__ __forceinline__ int64_t stair_G(const Grid& g, int64_t x, int a) {
+  const int64_t d = (int64_t)g.t + g.c0 + (int64_t)(a - 1) * g.cs;
+  return stair_T(x - d, g.cs) - stair_T(-d, g.cs);
+}
+__device__ __forceinline__ int64_t super_prefix(const Grid& g, int64_t x, int ma, int mb) {
+  return stair_G(g, x, ma) - stair_G(g, x, mb);
+}
+// tile index -> (i, j) in super-column order over owned columns [mlo, mhi)
+__device__ void super_tile_ij(const Grid& g, int64_t idx, int mlo, int mhi, int sw, int& i,
+                              int& j) {
+  int ma = mlo;
+  for (;;) {
+    const int mb = min(mhi, ma + sw);
+    const int64_t cnt = super_prefix(g, g.p, ma, mb);
+    if (idx < cnt || mb >= mhi) {
+      int lo = 0, hi = g.p;  // largest row x with P(x) <= idx
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (super_prefix(g, mid, ma, mb) <= idx) lo = mid; else hi = mid;
+      }
+      i = lo;
+      j = g.owned_col(ma + (int)(idx - super_prefix(g, lo, ma, mb)));
+      return;
+    }
+    idx -= cnt;
+    ma = mb;
+  }
+}
 
 constexpr int SCHED = 4;  // work-item ring between the producer and the consumers
 
@@ -89,7 +149,8 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
   uint64_t* sfull = tempty + 2;
   uint64_t* sempty = sfull + SCHED;
   int* sitem = (int*)(sempty + SCHED);
-  uint32_t* tmem_slot = (uint32_t*)(sitem + SCHED);
+  int2* sij = (int2*)(sitem + SCHED);  // (i, j) of the item, computed once by the producer
+  uint32_t* tmem_slot = (uint32_t*)(sij + SCHED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = g.nb;
@@ -105,11 +166,11 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], EPI_WARPS);
     }
     for (int s = 0; s < SCHED; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 5);  // MMA warp + 4 epilogue warps release a slot
+      mbar_init(&sempty[s], 1 + EPI_WARPS);  // MMA warp + epilogue warps release a slot
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -125,17 +186,22 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
   const uint32_t tmem_base = *tmem_slot;
 
   auto item_ij = [&](int item, int& i, int& j, int& m0, int& n0) {
-    const int64_t slot = w.slot0 + item / nsub;
+    const int64_t tile = item / nsub;
     const int sub = item % nsub;
-    g.off_slot_ij(slot, i, j);
+    if (!TRSM && w.sw > 0) super_tile_ij(g, tile, w.mlo, w.mhi, w.sw, i, j);
+    else g.off_slot_ij(w.slot0 + tile, i, j);
     m0 = (sub / w.nsubn) * BM;
     n0 = (sub % w.nsubn) * BN;
   };
-  // consumers read the li-th work item from the ring (-1 = no more work)
-  auto next_item = [&](uint32_t li) {
+  // consumers read the li-th work item (and its tile) from the ring (-1 = no more work)
+  auto next_item = [&](uint32_t li, int2* ij) {
     const int s = li % SCHED;
     mbar_wait(&sfull[s], (li / SCHED) & 1);
     const int item = *(volatile int*)&sitem[s];
+    if (ij) {
+      ij->x = *(volatile int*)&sij[s].x;
+      ij->y = *(volatile int*)&sij[s].y;
+    }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&sempty[s]);
     return item;
@@ -161,11 +227,20 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
           item = atomicAdd(w.counter, 1);
           if (item >= w.nitems) item = -1;
         }
+        int i = 0, j = 0, m0 = 0, n0 = 0;
+        if (item >= 0) item_ij(item, i, j, m0, n0);
         sitem[s] = item;
-        mbar_arrive(&sfull[s]);  // release: consumers see sitem[s]
+        sij[s] = make_int2(i, j);
+        mbar_arrive(&sfull[s]);  // release: consumers see sitem[s], sij[s]
         if (item < 0) break;
-        int i, j, m0, n0;
-        item_ij(item, i, j, m0, n0);
+        if (!TRSM && w.l2pf) {
+          // stage this item's C block (128 rows x 1 KB) in L2: the epilogue reads
+          // it one item later, so its loads hit L2 instead of waiting on HBM
+          const float* crow = g.stile(i, j) + (int64_t)m0 * nb + n0;
+          for (int r = 0; r < BM; ++r, crow += nb)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(crow), "r"(BN * 4)
+                         : "memory");
+        }
         // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb;
         // TRSM: A = pre-split of B_ik, B = split of W = L_kk^{-1}
         const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
@@ -188,7 +263,7 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
     // ------------------------------------------------ MMA issuer
     uint32_t it = 0;
     for (uint32_t li = 0;; ++li) {
-      const int item = next_item(li);
+      const int item = next_item(li, nullptr);
       if (item < 0) break;
       const int ksteps = item_ksteps(item);
       const uint32_t b = li & 1, aph = (li >> 1) & 1;
@@ -222,19 +297,42 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2..5)
+    // C is read from HBM one 32x32 chunk ahead of its use, the first chunk
+    // before the accumulator wait, so the load latency overlaps the MMAs
+    // instead of pacing them.
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
+    const int c_lo = EPI_WARPS == 4 ? 0 : ((warp - 2) / 4) * EPI_COLS;  // column range of this warp
     for (uint32_t li = 0;; ++li) {
-      const int item = next_item(li);
+      int2 ij;
+      const int item = next_item(li, &ij);
       if (item < 0) break;
-      int i, j, m0, n0;
-      item_ij(item, i, j, m0, n0);
+      const int i = ij.x, j = ij.y;
+      const int sub = item % nsub;
+      const int m0 = (sub / w.nsubn) * BM, n0 = (sub % w.nsubn) * BN;
       const uint32_t b = li & 1, aph = (li >> 1) & 1;
-      mbar_wait(&tfull[b], aph);
-      asm volatile("tcgen05.fence::after_thread_sync;");
       // rows q*32 .. q*32+31 of the 128x256 item; lane owns row q*32+lane in TMEM
       const int64_t roff = (int64_t)(m0 + q * 32) * nb + n0;
       float* cbase = g.stile(i, j) + roff;
+      float cn[32];
+      const int diag = w.diag;
+      if constexpr (!TRSM) {
+        if (!(diag & 1)) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) cn[r] = cbase[(int64_t)r * nb + c_lo + lane];
+        } else {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) cn[r] = 0.0f;
+        }
+      }
+      mbar_wait(&tfull[b], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (diag & 4) {
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+        continue;
+      }
       // split outputs: TRSM -> the panel split read by this step's updates;
       // update of column k+1 -> the pre-TRSM split of the next panel
       float* shi = TRSM ? g.split_hi(i, k) + roff
@@ -242,7 +340,7 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
       const int64_t te = g.tile_elems();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_lo + EPI_COLS; c += 32) {
         uint32_t v[32];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -260,32 +358,37 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
         for (int u = 0; u < 32; ++u) stg[lane * EPI_STRIDE + u] = __uint_as_float(v[u]);
         __syncwarp();
         float* cp = cbase + c + lane;
-        float* hp = shi ? shi + c + lane : nullptr;
+        float cv[32];
+        if constexpr (TRSM) {
 #pragma unroll
-        for (int r0 = 0; r0 < 32; r0 += 16) {  // 16 rows in flight per lane
-          float cv[16];
-          if (TRSM) {
+          for (int r = 0; r < 32; ++r) cv[r] = stg[r * EPI_STRIDE + lane];
+        } else {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) cv[r] = stg[(r0 + r) * EPI_STRIDE + lane];
-          } else {
+          for (int r = 0; r < 32; ++r) cv[r] = cn[r];
+          if (c + 32 < c_lo + EPI_COLS && !(diag & 1)) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) cv[r] = cp[(int64_t)(r0 + r) * nb];
-#pragma unroll
-            for (int r = 0; r < 16; ++r) cv[r] -= stg[(r0 + r) * EPI_STRIDE + lane];
+            for (int r = 0; r < 32; ++r) cn[r] = cp[(int64_t)r * nb + 32];
           }
 #pragma unroll
-          for (int r = 0; r < 16; ++r) cp[(int64_t)(r0 + r) * nb] = cv[r];
-          if (hp) {
-            float* hrow = hp + (int64_t)r0 * nb;
+          for (int r = 0; r < 32; ++r) cv[r] -= stg[r * EPI_STRIDE + lane];
+        }
+        if (!(diag & 2)) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-              uint32_t h;
-              asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(cv[r]));
-              asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(__uint_as_float(h)) : "memory");
-              asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(cv[r] - __uint_as_float(h))
-                           : "memory");
-              hrow += nb;
-            }
+          for (int r = 0; r < 32; ++r) cp[(int64_t)r * nb] = cv[r];
+        } else if (cv[0] == 1.2345f) {
+          cp[0] = cv[31];  // keep the arithmetic live
+        }
+        if (shi) {
+          float* hrow = shi + c + lane;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            uint32_t h;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(cv[r]));
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(__uint_as_float(h)) : "memory");
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(cv[r] - __uint_as_float(h))
+                         : "memory");
+            asm volatile("" : "+l"(hrow));  // keep one running row pointer (no hoisted addresses)
+            hrow += nb;
           }
         }
         __syncwarp();
@@ -375,8 +478,12 @@ bool mt_tc_trsm_enabled(const Grid& g) {
 namespace {
 // persistent launch over `nitems` work items of slot range [s0, s0 + scnt)
 int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
-                cudaStream_t st) {
+                cudaStream_t st, int jlo = 0, int jhi = 0) {
   if (scnt <= 0) return MT_OK;
+  if (mt_opt_cta_pairs() && !mt_opt_tc_diag() && !mt_opt_c_prefetch() &&
+      (trsm || mt_opt_super_cols() == 0))  // CTA-pair kernel (tc2_update.cu): slot order only
+    return mt_tc2_launch(g, k, s0, scnt, ctas, trsm,
+                         (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st);
   CUtensorMap ma, mb;
   const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;  // whole split buffer
   int rc = make_map(&ma, g.split, split_rows, g.nb, BM);
@@ -388,6 +495,11 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
   w.nsubn = g.nb / BN;
   w.nitems = (int)(scnt * w.nsubm * w.nsubn);
   w.presplit = (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0;
+  w.mlo = g.owned_before(jlo);
+  w.mhi = g.owned_before(jhi);
+  w.sw = (!trsm && jhi > jlo) ? mt_opt_super_cols() : 0;
+  w.l2pf = trsm ? 0 : mt_opt_c_prefetch();
+  w.diag = trsm ? 0 : mt_opt_tc_diag();
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_sm_count) cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
@@ -404,7 +516,7 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
   int grid = ctas > 0 ? ctas : g_sm_count;
   if (!trsm && g.yield && ctas <= 0) grid = 2 * g_sm_count;  // room to refill yielded SMs
   if (grid > w.nitems) grid = w.nitems;
-  const size_t smem = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  const size_t smem = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256 + SCHED * 8;
   if (trsm) {
     cudaFuncSetAttribute(tc32_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     tc32_trsm_kernel<<<grid, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
@@ -419,8 +531,9 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
 }  // namespace
 
 // FP32 updates of step k into off-band slots [s0, s0+scnt) via tcgen05; `ctas` caps the grid.
-int mt_tc_update_impl(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st) {
-  return launch_tc32(g, k, s0, scnt, ctas, false, st);
+int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st) {
+  const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
+  return launch_tc32(g, k, s0, scnt, ctas, false, st, jlo, jhi);
 }
 
 // Off-band panel TRSM of step k: X_ik = B_ik W^T for the off-band rows of

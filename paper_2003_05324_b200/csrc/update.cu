@@ -429,7 +429,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
       // the panel-column update (jhi == jlo + 1) runs beside the bulk update:
       // keep it narrow; the bulk update may be capped to leave SMs for the panel
       const int ctas = (jhi == jlo + 1) ? mt_opt_pcol_ctas() : mt_opt_update_ctas();
-      return mt_tc_update_impl(g, k, s0, scnt, ctas, st);
+      return mt_tc_update_impl(g, k, jlo, jhi, ctas, st);
     }
     if (nb % SBM == 0) {
       const int nsub = nb / SBM;

