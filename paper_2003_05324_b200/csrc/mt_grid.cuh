@@ -143,6 +143,30 @@ inline Grid make_grid(const mt_tiles* g) {
   return r;
 }
 
+// TF32 hi/lo split of an FP32 operand for 3xTF32 products: hi = rna_tf32(x)
+// (exact in TF32), lo = x - hi (exact in FP32, so hi + lo == x: the multi-GPU
+// DMMA band update rebuilds the FP32 payload from a received split).  The MMA
+// reads only lo's TF32 bits; lo's sign is random, so that truncation is
+// unbiased.  MT_LO_RNA=1 rounds lo to TF32 instead -- measured on B200
+// (tools/acc_tf32.py) to change the factor error by < 1.3x either way, so the
+// exact split is kept.
+#ifndef MT_LO_RNA
+#define MT_LO_RNA 0
+#endif
+__device__ __forceinline__ void mt_tf32_split(float x, float& hi, float& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  const float r = x - hi;
+#if MT_LO_RNA
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  lo = __uint_as_float(l);
+#else
+  lo = r;
+#endif
+}
+
 // status slots
 #define MT_ST_PIVOT 0
 #define MT_ST_OVERFLOW 1

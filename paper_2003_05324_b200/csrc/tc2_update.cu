@@ -24,9 +24,9 @@
 //           as in tc_update.cu; they release the accumulator on the leader's
 //           `tempty` (4 local + 4 remote arrivals).
 // Every output element is produced by one pair per step with the same MMA
-// sequence as a function of its position only: deterministic and
-// schedule-invariant (bitwise equal to the single-CTA kernel is NOT claimed:
-// the K-slab order is the same, so it is, but tests check it explicitly).
+// sequence (K slabs in order, lo*hi, hi*lo, hi*hi) as in the single-CTA
+// kernel: deterministic, schedule-invariant, and bit-identical to it
+// (tests/test_gpu_tc.py::test_cta_pair_kernel_bitwise_equals_single_cta).
 #include <cuda.h>
 
 #include "tma.cuh"
@@ -355,11 +355,10 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
           float* hrow = shi + c + lane;
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
-            uint32_t h;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(cv[r]));
-            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(__uint_as_float(h)) : "memory");
-            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(cv[r] - __uint_as_float(h))
-                         : "memory");
+            float h, l;
+            mt_tf32_split(cv[r], h, l);
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(h) : "memory");
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(l) : "memory");
             asm volatile("" : "+l"(hrow));
             hrow += nb;
           }

@@ -5,9 +5,10 @@
 // FP32 products are emulated with three TF32 UMMAs per K-step,
 //   A B^T ~= A_lo B_hi^T + A_hi B_lo^T + A_hi B_hi^T,
 // hi = cvt.rna.tf32(x) (exactly representable in TF32), lo = x - hi (exact
-// in FP32).  The dropped A_lo B_lo term and the TF32 truncation of lo are
-// O(2^-22) relative, i.e. FP32-class accuracy (checked against the FFMA
-// kernel and the CPU reference in tests/test_gpu_tc.py).  The hi/lo split is
+// in FP32; Grid-level helper mt_tf32_split).  The dropped A_lo B_lo term and
+// the TF32 truncation of lo are O(2^-22) relative, i.e. FP32-class accuracy:
+// measured factor error vs the CPU reference 0.4-0.95x that of the SIMT FFMA
+// kernel (tools/acc_tf32.py; bounded in tests/test_gpu_tc.py).  The hi/lo split is
 // produced once per panel tile by the TRSM epilogue (Grid::split_hi/lo), so
 // the update streams both halves straight from L2 with TMA -- no per-stage
 // conversion through the LSU pipe.
@@ -382,11 +383,10 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
           float* hrow = shi + c + lane;
 #pragma unroll
           for (int r = 0; r < 32; ++r) {
-            uint32_t h;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(cv[r]));
-            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(__uint_as_float(h)) : "memory");
-            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(cv[r] - __uint_as_float(h))
-                         : "memory");
+            float h, l;
+            mt_tf32_split(cv[r], h, l);
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow), "f"(h) : "memory");
+            asm volatile("st.global.f32 [%0], %1;" ::"l"(hrow + te), "f"(l) : "memory");
             asm volatile("" : "+l"(hrow));  // keep one running row pointer (no hoisted addresses)
             hrow += nb;
           }

@@ -193,10 +193,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (M) M[o] = f;
       if (DP) DP[o] = (double)v;  // multi-GPU: FP64 band panel row for the broadcast
       if (SH) {
-        uint32_t h;
-        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
-        SH[o] = __uint_as_float(h);
-        SL[o] = f - __uint_as_float(h);
+        float h, l;
+        mt_tf32_split(f, h, l);
+        SH[o] = h;
+        SL[o] = l;
       }
     }
   }
@@ -339,11 +339,11 @@ __global__ void __launch_bounds__(128) trinv_kernel(Grid g, int k) {
     const int R = e / TW, c = e % TW;
     const double w = R >= cb * 32 ? Wc[R * TW + c] : 0.0;
     const float f = __double2float_rn(w);
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(f));
+    float h, l;
+    mt_tf32_split(f, h, l);
     const int64_t o = (int64_t)R * nb + c0 + c;
-    WH[o] = __uint_as_float(h);
-    WL[o] = f - __uint_as_float(h);
+    WH[o] = h;
+    WL[o] = l;
   }
 }
 
@@ -364,12 +364,7 @@ __global__ void __launch_bounds__(256) presplit_kernel(Grid g, int k, int64_t s0
     float* hp = (float*)&h;
     float* lp = (float*)&l;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      uint32_t b;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(xp[u]));
-      hp[u] = __uint_as_float(b);
-      lp[u] = xp[u] - hp[u];
-    }
+    for (int u = 0; u < 4; ++u) mt_tf32_split(xp[u], hp[u], lp[u]);
     hi[e] = h;
     lo[e] = l;
   }
