@@ -71,6 +71,10 @@ __device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cl_relaxed(uint32_t cl_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -183,14 +187,18 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
     const int s = li % SCHED;
     mbar_wait_cl(&sfull[s], (li / SCHED) & 1);
     const int item = *(volatile int*)&sitem[s];
+    int dep = item;
     if (pi) {
       *pi = *(volatile int*)&si[s];
       *pj = *(volatile int*)&sj[s];
+      dep ^= *pi ^ *pj;
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) {
-      if (leader) mbar_arrive(&sempty[s]);
-      else mbar_arrive_cl(peer_addr(&sempty[s], 0));
+    // release the slot with a relaxed arrive (no fence on this warp's pending C
+    // stores); the shuffle makes the arrive depend on every lane's loaded values
+    dep = __reduce_xor_sync(0xffffffffu, dep);
+    if ((threadIdx.x & 31) == 0 && dep != 0x7fffffff) {
+      if (leader) mbar_arrive_relaxed(&sempty[s]);
+      else mbar_arrive_cl_relaxed(peer_addr(&sempty[s], 0));
     }
     return item;
   };
@@ -229,7 +237,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
           item = *(volatile int*)&sitem[s];
           i = *(volatile int*)&si[s];
           j = *(volatile int*)&sj[s];
-          mbar_arrive_cl(peer_addr(&sempty[s], 0));
+          if ((item ^ i ^ j) != 0x7fffffff) mbar_arrive_cl_relaxed(peer_addr(&sempty[s], 0));
         }
         if (item < 0) break;
         const int sub = item % nsub;
@@ -367,7 +375,8 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) mbar_arrive_cl(tempty_leader[b]);
+      // TMEM reads completed (tcgen05.wait::ld): relaxed arrive, no wait on the C stores
+      if (lane == 0) mbar_arrive_cl_relaxed(tempty_leader[b]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

@@ -199,12 +199,15 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
     const int s = li % SCHED;
     mbar_wait(&sfull[s], (li / SCHED) & 1);
     const int item = *(volatile int*)&sitem[s];
+    int dep = item;
     if (ij) {
       ij->x = *(volatile int*)&sij[s].x;
       ij->y = *(volatile int*)&sij[s].y;
+      dep ^= ij->x ^ ij->y;
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&sempty[s]);
+    // relaxed release of the slot, dependent on every lane's loaded values
+    dep = __reduce_xor_sync(0xffffffffu, dep);
+    if ((threadIdx.x & 31) == 0 && dep != 0x7fffffff) mbar_arrive_relaxed(&sempty[s]);
     return item;
   };
 
@@ -395,7 +398,7 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
+      if (lane == 0) mbar_arrive_relaxed(&tempty[b]);  // TMEM reads done; C stores need no fence
     }
   }
   __syncthreads();

@@ -22,6 +22,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// relaxed arrive: no release fence, so it does not wait for this thread's
+// outstanding global stores (a default .release arrive compiles to
+// MEMBAR.ALL.CTA, which stalls an epilogue warp on its own C stores).  Use only
+// where the barrier orders on-chip state (TMEM reads finished via
+// tcgen05.wait::ld, or smem reads whose values the caller already consumed).
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* b) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   do {
