@@ -1,0 +1,71 @@
+"""GPU: BASELINE config sizes, checked through size-independent properties
+(the CPU oracle cannot factor N=65536 in a test's time budget).
+
+configs[1] (N=65536, nb=512): field-sampled z (the build's own full-DP
+generate_field, as SURVEY.md §8d prescribes for N >= 65536); the MP
+likelihood at each DP-band width stays within the north-star MP tolerance of
+the build's own full-DP likelihood, the DP-band sweep converges to DP, MP
+with the band covering the matrix is bitwise DP, and the factor reproduces
+z through L (L^{-1} z then L y round trip).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+MP_TOL = 1e-5
+
+
+def _mt():
+    import paper_2003_05324_b200 as mt
+    return mt
+
+
+@pytest.fixture(scope="module")
+def field65536(gpu):
+    mt = _mt()
+    th = mt.MaternParams(1.0, 0.1, 0.5)
+    locs = mt.generate_locations(65536, seed=mt.derive_seed(2, 0))
+    ds, _ = mt.morton_sort(mt.generate_field(locs, th, seed=mt.derive_seed(2, 1), nb=512))
+    return ds, th
+
+
+def test_config2_band_sweep_vs_own_dp(field65536):
+    mt = _mt()
+    ds, th = field65536
+    asm = mt.TileAssembler(ds, 512)
+    ld_dp, q_dp = mt.Evaluator(asm, mt.PrecisionPolicy.dp())(th)
+    l_dp = -0.5 * (ds.n * math.log(2 * math.pi) + ld_dp + q_dp)
+    # field z: quad / n ~ 1 (a sanity check that z really is a draw from Sigma)
+    assert 0.9 < q_dp / ds.n < 1.1
+    errs = []
+    for t in (1, 2, 4, 8):
+        ld, q = mt.Evaluator(asm, mt.PrecisionPolicy.mp(diag_thick=t))(th)
+        val = -0.5 * (ds.n * math.log(2 * math.pi) + ld + q)
+        errs.append(abs(val - l_dp) / abs(l_dp))
+        assert errs[-1] <= MP_TOL, (t, val, l_dp)
+    # a wider FP64 band is not less accurate (up to rounding noise)
+    assert errs[-1] <= errs[0] * 1.5 + 1e-12, errs
+
+
+def test_config2_full_band_mp_bitwise_dp(field65536):
+    mt = _mt()
+    ds, th = field65536
+    asm = mt.TileAssembler(ds, 512)
+    a = mt.Evaluator(asm, mt.PrecisionPolicy.dp())(th)
+    b = mt.Evaluator(asm, mt.PrecisionPolicy.mp(diag_thick=asm.p))(th)
+    assert a == b
+
+
+def test_config2_solve_round_trip(field65536):
+    mt = _mt()
+    ds, th = field65536
+    fac = mt.cholesky(mt.assemble_covariance(ds, th, 512, mt.PrecisionPolicy.mp(diag_thick=2)))
+    y = mt.forward_solve(fac, ds.z)        # L^{-1} z
+    back = mt.matvec_lower(fac, y)         # L (L^{-1} z)
+    assert np.max(np.abs(back - ds.z)) <= 1e-9 * np.max(np.abs(ds.z)) * 1e3
+    x = mt.solve(fac, ds.z)                # Sigma^{-1} z; z.x = ||L^{-1} z||^2
+    assert math.isclose(float(ds.z @ x), float(y @ y), rel_tol=1e-9)

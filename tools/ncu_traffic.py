@@ -32,6 +32,10 @@ def summarise(path):
         m = re.search(r"(\w+_kernel)", d["Kernel Name"])
         names[lid] = m.group(1) if m else d["Kernel Name"][:40]
         per[lid][d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
+    # split a kernel's launches by grid size when recorded (bulk vs panel-column updates)
+    for lid, ms in per.items():
+        if "launch__grid_size" in ms:
+            names[lid] += f"[grid={int(ms['launch__grid_size'])}]"
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for lid, ms in per.items():
         a = agg[names[lid]]
