@@ -248,8 +248,11 @@ bool mt_dmma_tma_supported(const Grid& g) {
          (int64_t)g.noff() * g.nb < (1ll << 31) && (int64_t)4 * g.p * g.nb < (1ll << 31);
 }
 
-// band updates of step k into band slots [b0, b0 + bcnt)
-int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st) {
+// band updates of step k into band slots [b0, b0 + bcnt).  pdl: launch as a
+// programmatic dependent of the previous kernel on `st` (the capped bulk FP32
+// update, which writes disjoint tiles): it starts on the SMs that update left
+// free instead of after it.
+int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st, bool pdl) {
   if (bcnt <= 0) return MT_OK;
   const int nb = g.nb;
   Maps maps;
@@ -267,7 +270,23 @@ int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStre
   if (rc) return rc;
   const int nsm = nb / BM, nsn = nb / BN;
   cudaFuncSetAttribute(dmma_tma_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-  dmma_tma_update_kernel<<<(unsigned)(bcnt * nsm * nsn), 256, SMEM, st>>>(g, k, b0, nsm, nsn, maps);
+  if (!pdl) {
+    dmma_tma_update_kernel<<<(unsigned)(bcnt * nsm * nsn), 256, SMEM, st>>>(g, k, b0, nsm, nsn, maps);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(bcnt * nsm * nsn));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (mt_cuda_check(cudaLaunchKernelEx(&cfg, dmma_tma_update_kernel, g, k, b0, nsm, nsn, maps),
+                      "dmma_tma_update_kernel (PDL)"))
+      return MT_E_CUDA;
+  }
   MT_LAUNCH_CHECK("dmma_tma_update_kernel");
   return MT_OK;
 }

@@ -207,7 +207,9 @@ int mt_opt_legacy_dmma();
 int mt_opt_pcol_ctas();
 int mt_opt_yield_sms();
 bool mt_dmma_tma_supported(const Grid& g);
-int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st);
+int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st,
+                        bool pdl = false);
+int mt_opt_coschedule();
 bool mt_tc_supported(const Grid& g);
 bool mt_tc_trsm_enabled(const Grid& g);  // off-band TRSM as a tcgen05 GEMM against L_kk^{-1}
 int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st);

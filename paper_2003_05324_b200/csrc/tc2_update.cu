@@ -143,6 +143,9 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
   uint32_t* tmem_slot = (uint32_t*)(sj + SCHED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // co-scheduled band update (option 10): once every pair of this grid is
+  // resident, a programmatic-dependent DMMA launch may take the SMs left over
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int nb = g.nb;

@@ -389,6 +389,9 @@ static void update_flops(const Grid& g, int k, int jlo, int jhi, double& f64, do
   }
 }
 
+#define RC_UPD(call) \
+  do { int rc__ = (call); if (rc__) return rc__; } while (0)
+
 int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   if (jlo >= jhi) return MT_OK;
   const int nb = g.nb;
@@ -399,6 +402,35 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   double f64, f32;
   update_flops(g, k, jlo, jhi, f64, f32);
   const bool pcol = (jlo == k + 1 && jhi == jlo + 1 && jhi < g.p);  // lookahead panel column
+  // Co-scheduling (option 10): the bulk FP32 update runs on a capped set of
+  // SM pairs and the FP64 band update is launched as its programmatic
+  // dependent, filling the remaining SMs -- DMMA work (low power) then runs
+  // beside the power-capped tensor-core work instead of after it.  The split
+  // follows the step's FP64/FP32 work at the measured pipe rates; the band
+  // update gets slightly less than its share so it, not the capped FP32
+  // update, absorbs the tail (its CTAs spread onto the SMs the update frees).
+  const int64_t co_s0 = g.scol(jlo), co_scnt = g.scol(jhi) - co_s0;
+  const int64_t co_b0 = g.bcol(jlo), co_bcnt = g.bcol(jhi) - co_b0;
+  if (mt_opt_coschedule() && !pcol && g.mode == MT_MODE_MP && co_scnt > 0 && co_bcnt > 0 &&
+      (mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) && mt_tc_supported(g) &&
+      mt_opt_cta_pairs() && mt_opt_legacy_dmma() != 1 && mt_dmma_tma_supported(g)) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const double a = f64 / 32e12, b = f32 / 215e12;  // seconds on the whole GPU
+    int x = (int)(0.9 * sms * a / (a + b));          // SMs left to the band update
+    int tc_ctas = (sms - x) & ~1;
+    if (tc_ctas < 2) tc_ctas = 2;
+    // one profiling span for the pair (an event between the two launches would
+    // serialise them): kind upd32, flops of both
+    ProfScope ps(MT_K_UPD32, st, f32 + f64,
+                 co_scnt * (double)nb * nb * 4.0 * 2.0 + co_bcnt * (double)nb * nb * 8.0 * 3.0, 2);
+    RC_UPD(mt_tc_update_impl(g, k, jlo, jhi, tc_ctas, st));
+    return mt_dmma_update_impl(g, k, co_b0, co_bcnt, st, true);
+  }
   // band (FP64) outputs in columns [jlo, jhi)
   const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
   if (bcnt > 0) {

@@ -215,3 +215,25 @@ def test_cta_pair_kernel_bitwise_equals_single_cta(gpu, n, nb, t, ysms):
     for key in facs[0].tiles:
         a, b = facs[0].tiles[key], facs[1].tiles[key]
         assert np.array_equal(a.dp, b.dp), key
+
+
+@pytest.mark.parametrize("n,nb,t", [(8192, 512, 3), (6144, 256, 2)])
+def test_coscheduled_band_update_bitwise(gpu, n, nb, t):
+    """Option 10 (FP64 band update launched as a programmatic dependent beside a
+    capped FP32 update) changes only where and when work runs: bitwise equal."""
+    mt = _mt()
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    locs = mt.generate_locations(n, seed=29)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    pol = mt.PrecisionPolicy.mp(diag_thick=t)
+    facs = []
+    for co in (0, 1):
+        old = lib.mt_set_option(10, co)
+        try:
+            facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), nb,
+                                                           pol), lookahead=1))
+        finally:
+            lib.mt_set_option(10, old)
+    for key in facs[0].tiles:
+        assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
