@@ -230,6 +230,11 @@ int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t, const doubl
 long long mt_launch_count(void);
 int mt_prof_begin(int32_t capacity);
 int mt_prof_end(int32_t nkinds, double* ms, double* flops, double* bytes, int64_t* count);
+/* After mt_prof_end: per kind, sum of ms x (fraction of the SMs each launch was
+ * given).  Launches that overlap another kernel by design (the FP32 bulk update
+ * co-scheduled with the band update, option 10) time themselves on the device
+ * (%globaltimer spans) and run on a share of the SMs. */
+int mt_prof_sm_weighted(int32_t nkinds, double* ms_w);
 
 /* Peak probes for roofline denominators: kind 0 FFMA, 1 DFMA, 2 FP64 DMMA;
  * *tflops = achieved TFLOP/s of a dependent-chain FMA kernel on all SMs. */
@@ -250,7 +255,10 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   8: diagnostics of the FP32 update epilogue (timing only, WRONG results):
  *      bit 0 skip C loads, bit 1 skip C stores, bit 2 skip the epilogue
  *   9: 1 = FP32 update and off-band TRSM on CTA pairs (tcgen05.mma.cta_group::2,
- *      M = 256, each CTA stages half of B; default), 0 = single-CTA kernel */
+ *      M = 256, each CTA stages half of B; default), 0 = single-CTA kernel
+ *  10: 1 = co-schedule the FP64 band update (programmatic dependent launch) on the
+ *      SMs a capped bulk FP32 update leaves free (default), 0 = one after the other
+ *  11: band update's SM share under option 10, in % of its work share (default 90) */
 int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */

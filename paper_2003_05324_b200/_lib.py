@@ -98,6 +98,7 @@ SIGNATURES = {
     "mt_launch_count": (ctypes.c_longlong, []),
     "mt_prof_begin": (ctypes.c_int, [_I32]),
     "mt_prof_end": (ctypes.c_int, [_I32, _V, _V, _V, _V]),
+    "mt_prof_sm_weighted": (ctypes.c_int, [_I32, _V]),
     "mt_peak_probe": (ctypes.c_int, [_I32, _I32, _P(_D)]),
     "mt_evaluate_host": (ctypes.c_int, [_I64, _I32, _I32, _I32, _V, _V, _I32, _D, _P(MtMatern),
                                         _V, _P(_I64)]),

@@ -168,7 +168,8 @@ __device__ __forceinline__ void mainloop(const unsigned char* smem, uint64_t* fu
 
 __global__ void __launch_bounds__(256, 2)
     dmma_tma_update_kernel(Grid g, int k, int64_t slot0, int nsubm, int nsubn,
-                           const __grid_constant__ Maps maps) {
+                           const __grid_constant__ Maps maps, unsigned long long* span) {
+  if (span && threadIdx.x == 0) atomicMin(&span[0], mt_globaltimer());
   if (g.failed()) return;
   const int nsub = nsubm * nsubn;
   const int64_t slot = slot0 + blockIdx.x / nsub;
@@ -239,6 +240,10 @@ __global__ void __launch_bounds__(256, 2)
       else if (c <= r) C[(int64_t)r * nb + c] = v.x;
     }
   }
+  if (span) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&span[1], mt_globaltimer());
+  }
 }
 
 }  // namespace
@@ -252,7 +257,8 @@ bool mt_dmma_tma_supported(const Grid& g) {
 // programmatic dependent of the previous kernel on `st` (the capped bulk FP32
 // update, which writes disjoint tiles): it starts on the SMs that update left
 // free instead of after it.
-int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st, bool pdl) {
+int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st, bool pdl,
+                        unsigned long long* span) {
   if (bcnt <= 0) return MT_OK;
   const int nb = g.nb;
   Maps maps;
@@ -271,7 +277,8 @@ int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStre
   const int nsm = nb / BM, nsn = nb / BN;
   cudaFuncSetAttribute(dmma_tma_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   if (!pdl) {
-    dmma_tma_update_kernel<<<(unsigned)(bcnt * nsm * nsn), 256, SMEM, st>>>(g, k, b0, nsm, nsn, maps);
+    dmma_tma_update_kernel<<<(unsigned)(bcnt * nsm * nsn), 256, SMEM, st>>>(g, k, b0, nsm, nsn, maps,
+                                                                             span);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(bcnt * nsm * nsn));
@@ -283,7 +290,7 @@ int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (mt_cuda_check(cudaLaunchKernelEx(&cfg, dmma_tma_update_kernel, g, k, b0, nsm, nsn, maps),
+    if (mt_cuda_check(cudaLaunchKernelEx(&cfg, dmma_tma_update_kernel, g, k, b0, nsm, nsn, maps, span),
                       "dmma_tma_update_kernel (PDL)"))
       return MT_E_CUDA;
   }

@@ -132,6 +132,56 @@ struct Grid {
   }
 };
 
+// ---- L2-friendly output order of the trailing update -----------------------
+// Slot order (column by column) re-reads every row operand A_ik from HBM once
+// per output column: at p - k = 500 the panel split (2 MB per tile) is far
+// larger than L2.  Instead the outputs are visited in super-columns of `sw`
+// owned columns, rows ascending inside each, columns ascending inside a row:
+// a row operand is then fetched once per super-column and the sw column
+// operands stay L2-resident while the rows sweep past.  Every output tile is
+// still computed by exactly one work item, so results do not depend on it.
+//
+// Owned column m is global column j = c0 + m*cs; its off-band rows are
+// i in [j + t, p).  In a super-column [ma, mb) row i holds the columns
+// m in [ma, min(mb, F(i) + 1)), F(i) = floor((i - t - c0) / cs), so the tiles
+// before row x number P(x) = G(x, ma) - G(x, mb) with
+// G(x, a) = sum_{i<x} max(0, floor((i - d_a) / cs)), d_a = t + c0 + (a - 1) cs,
+// = T(x - d_a) - T(-d_a),  T(Y) = sum_{y<Y} floor(y / cs)  (0 for Y <= 0).
+__device__ __forceinline__ int64_t stair_T(int64_t y, int cs) {
+  if (y <= 0) return 0;
+  const int64_t q = y / cs, r = y % cs;
+  return (int64_t)cs * q * (q - 1) / 2 + r * q;
+}
+__device__ __forceinline__ int64_t stair_G(const Grid& g, int64_t x, int a) {
+  const int64_t d = (int64_t)g.t + g.c0 + (int64_t)(a - 1) * g.cs;
+  return stair_T(x - d, g.cs) - stair_T(-d, g.cs);
+}
+__device__ __forceinline__ int64_t super_prefix(const Grid& g, int64_t x, int ma, int mb) {
+  return stair_G(g, x, ma) - stair_G(g, x, mb);
+}
+// tile index -> (i, j) in super-column order over owned columns [mlo, mhi)
+__device__ __forceinline__ void super_tile_ij(const Grid& g, int64_t idx, int mlo, int mhi, int sw, int& i,
+                              int& j) {
+  int ma = mlo;
+  for (;;) {
+    const int mb = min(mhi, ma + sw);
+    const int64_t cnt = super_prefix(g, g.p, ma, mb);
+    if (idx < cnt || mb >= mhi) {
+      int lo = 0, hi = g.p;  // largest row x with P(x) <= idx
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (super_prefix(g, mid, ma, mb) <= idx) lo = mid; else hi = mid;
+      }
+      i = lo;
+      j = g.owned_col(ma + (int)(idx - super_prefix(g, lo, ma, mb)));
+      return;
+    }
+    idx -= cnt;
+    ma = mb;
+  }
+}
+
+
 inline Grid make_grid(const mt_tiles* g) {
   Grid r;
   r.n = g->n; r.nb = g->nb; r.p = g->p; r.t = g->t; r.mode = g->mode;
@@ -188,6 +238,14 @@ enum MtKind {
   MT_K_UPD64P, MT_K_UPD32P,  // lookahead panel-column updates (step k -> column k+1)
   MT_NKINDS
 };
+// device-side span slot [start, end] (ns, %globaltimer) for a kernel that cannot be
+// bracketed by stream events; nullptr when not profiling
+unsigned long long* mt_prof_dspan(int kind, double flops, double bytes, double share = 1.0);
+__device__ __forceinline__ unsigned long long mt_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 // brackets the launches of one kernel group with profiling events
 struct ProfScope {
   int tok;
@@ -208,16 +266,19 @@ int mt_opt_pcol_ctas();
 int mt_opt_yield_sms();
 bool mt_dmma_tma_supported(const Grid& g);
 int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStream_t st,
-                        bool pdl = false);
+                        bool pdl = false, unsigned long long* span = nullptr);
 int mt_opt_coschedule();
+int mt_opt_coschedule_pct();
 bool mt_tc_supported(const Grid& g);
 bool mt_tc_trsm_enabled(const Grid& g);  // off-band TRSM as a tcgen05 GEMM against L_kk^{-1}
 int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st);
 int mt_opt_tc_trsm();
-int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st);
+int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st,
+                      unsigned long long* span = nullptr);
 int mt_opt_super_cols();
 int mt_opt_c_prefetch();
 int mt_opt_tc_diag();
 int mt_opt_cta_pairs();
 int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
-                  int presplit, cudaStream_t st);
+                  int presplit, cudaStream_t st, unsigned long long* span = nullptr, int jlo = 0,
+                  int jhi = 0);

@@ -18,9 +18,19 @@
 namespace {
 struct Rec {
   int kind;
-  int ev;
+  int ev;      // event pair index, or -1 for a device-side span
+  int span;    // device span slot (ev < 0)
   double flops, bytes;
+  double share = 1.0;  // fraction of the SMs the launch was given (co-scheduled launches)
 };
+std::vector<double> g_ms_weighted;  // per kind: sum of ms * share of the last profiled region
+// Device-side kernel spans: a kernel that runs concurrently with another one
+// on the same stream (the co-scheduled band update is a programmatic
+// dependent launch) cannot be bracketed by stream events, so it stamps
+// %globaltimer itself: atomicMin(start), atomicMax(end) over its CTAs.
+unsigned long long* g_spans = nullptr;  // [capacity][2]
+int g_span_cap = 0;
+int g_next_span = 0;
 std::mutex g_mu;
 std::atomic<long long> g_launches{0};
 bool g_on = false;
@@ -37,8 +47,16 @@ int mt_prof_start(int kind, cudaStream_t st, double flops, double bytes) {
   int e = g_next_ev;
   g_next_ev += 2;
   cudaEventRecord(g_events[e], st);
-  g_recs.push_back({kind, e, flops, bytes});
+  g_recs.push_back({kind, e, -1, flops, bytes});
   return e;
+}
+
+unsigned long long* mt_prof_dspan(int kind, double flops, double bytes, double share) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (!g_on || !g_spans || g_next_span >= g_span_cap) return nullptr;
+  const int sl = g_next_span++;
+  g_recs.push_back({kind, -1, sl, flops, bytes, share});
+  return g_spans + 2 * sl;
 }
 
 void mt_prof_stop(int token, cudaStream_t st) {
@@ -97,6 +115,22 @@ int mt_prof_begin(int32_t capacity) {
   }
   g_recs.clear();
   g_next_ev = 0;
+  g_next_span = 0;
+  if (g_span_cap < capacity) {
+    if (g_spans) cudaFree(g_spans);
+    g_spans = nullptr;
+    g_span_cap = 0;
+    if (mt_cuda_check(cudaMalloc(&g_spans, sizeof(unsigned long long) * 2 * capacity), "span alloc"))
+      return MT_E_CUDA;
+    g_span_cap = capacity;
+  }
+  {  // start = ~0 (atomicMin target), end = 0 (atomicMax target)
+    std::vector<unsigned long long> init(2 * (size_t)g_span_cap);
+    for (size_t q = 0; q < init.size(); q += 2) { init[q] = ~0ull; init[q + 1] = 0ull; }
+    if (mt_cuda_check(cudaMemcpy(g_spans, init.data(), init.size() * sizeof(unsigned long long),
+                                 cudaMemcpyHostToDevice), "span init"))
+      return MT_E_CUDA;
+  }
   g_on = true;
   return MT_OK;
 }
@@ -106,17 +140,38 @@ int mt_prof_end(int32_t nkinds, double* ms, double* flops, double* bytes, int64_
   std::lock_guard<std::mutex> lock(g_mu);
   g_on = false;
   for (int k = 0; k < nkinds; ++k) { ms[k] = flops[k] = bytes[k] = 0.0; count[k] = 0; }
+  g_ms_weighted.assign(nkinds > 0 ? nkinds : 0, 0.0);
   if (mt_cuda_check(cudaDeviceSynchronize(), "prof sync")) return MT_E_CUDA;
+  std::vector<unsigned long long> spans(2 * (size_t)g_next_span);
+  if (g_next_span &&
+      mt_cuda_check(cudaMemcpy(spans.data(), g_spans, spans.size() * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost), "span read"))
+    return MT_E_CUDA;
   for (const Rec& r : g_recs) {
     if (r.kind < 0 || r.kind >= nkinds) continue;
     float t = 0.f;
-    if (cudaEventElapsedTime(&t, g_events[r.ev], g_events[r.ev + 1]) != cudaSuccess) continue;
+    if (r.ev < 0) {
+      const unsigned long long a = spans[2 * r.span], b = spans[2 * r.span + 1];
+      if (b < a) continue;  // kernel exited before stamping (e.g. failed pivot)
+      t = (float)((b - a) * 1e-6);
+    } else if (cudaEventElapsedTime(&t, g_events[r.ev], g_events[r.ev + 1]) != cudaSuccess) {
+      continue;
+    }
     ms[r.kind] += t;
+    g_ms_weighted[r.kind] += t * r.share;
     flops[r.kind] += r.flops;
     bytes[r.kind] += r.bytes;
     count[r.kind] += 1;
   }
   g_recs.clear();
+  return MT_OK;
+}
+
+// per kind, of the last mt_prof_end region: sum over launches of ms x (fraction of
+// the SMs the launch was given); equals ms for launches that had the whole GPU
+int mt_prof_sm_weighted(int32_t nkinds, double* ms_w) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (int k = 0; k < nkinds; ++k) ms_w[k] = k < (int)g_ms_weighted.size() ? g_ms_weighted[k] : 0.0;
   return MT_OK;
 }
 

@@ -41,9 +41,16 @@ constexpr int BK = 16, STAGES = 6;
 constexpr int A_BYTES = BM * BK * 4;  // 8 KB
 constexpr int B_BYTES = BNH * BK * 4; // 8 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
-constexpr int NUM_THREADS = 192;
+#ifndef MT_TC2_EPI
+#define MT_TC2_EPI 4
+#endif
+// epilogue warps per CTA: 4 (one per TMEM lane quadrant) or 8 (two per
+// quadrant, each on half of the item's columns: twice the C loads in flight)
+constexpr int EPI_WARPS = MT_TC2_EPI;
+constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int EPI_STRIDE = 33;
-constexpr int EPI_BYTES = 4 * 32 * EPI_STRIDE * 4;
+constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_STRIDE * 4;
 constexpr int TMEM_COLS = 512;        // 2 accumulators x 256 columns
 constexpr int SCHED = 4;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
@@ -123,6 +130,8 @@ struct Work2 {
   int nsubm, nsubn;
   int* counter;  // [work queue head, pairs started]
   int presplit;
+  unsigned long long* span;  // profiling: device-side [start, end] stamps (or null)
+  int mlo, mhi, sw;          // update: owned column range and super-column width (0 = slot order)
 };
 
 template <bool TRSM>
@@ -161,11 +170,11 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);  // leader: 4 local + 4 peer epilogue warps
+      mbar_init(&tempty[b], 2 * EPI_WARPS);  // leader: local + peer epilogue warps
     }
     for (int s = 0; s < SCHED; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 10);  // leader: MMA + 4 epi + peer producer + 4 peer epi
+      mbar_init(&sempty[s], 2 + 2 * EPI_WARPS);  // leader: MMA + epi + peer producer + peer epi
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -179,10 +188,12 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
   __syncthreads();
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;");
+  if (w.span && threadIdx.x == 0) atomicMin(&w.span[0], mt_globaltimer());
   const uint32_t tmem_base = *tmem_slot;
 
   auto tile_of = [&](int item, int& i, int& j) {
-    g.off_slot_ij(w.slot0 + item / nsub, i, j);
+    if (!TRSM && w.sw > 0) super_tile_ij(g, item / nsub, w.mlo, w.mhi, w.sw, i, j);
+    else g.off_slot_ij(w.slot0 + item / nsub, i, j);
   };
   // consumer side of the work ring (both CTAs); the peer releases the
   // leader's slot remotely
@@ -307,6 +318,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
     // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
+    const int c_lo = EPI_WARPS == 4 ? 0 : ((warp - 2) / 4) * EPI_COLS;  // this warp's columns
     const uint32_t tempty_leader[2] = {peer_addr(&tempty[0], 0), peer_addr(&tempty[1], 0)};
     for (uint32_t li = 0;; ++li) {
       int i, j;
@@ -320,7 +332,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       float cn[32];
       if constexpr (!TRSM) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) cn[r] = cbase[(int64_t)r * nb + lane];
+        for (int r = 0; r < 32; ++r) cn[r] = cbase[(int64_t)r * nb + c_lo + lane];
       }
       mbar_wait(&tfull[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -329,7 +341,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       const int64_t te = g.tile_elems();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_lo + EPI_COLS; c += 32) {
         uint32_t v[32];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -353,7 +365,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
         } else {
 #pragma unroll
           for (int r = 0; r < 32; ++r) cv[r] = cn[r];
-          if (c + 32 < BN) {
+          if (c + 32 < c_lo + EPI_COLS) {
 #pragma unroll
             for (int r = 0; r < 32; ++r) cn[r] = cp[(int64_t)r * nb + 32];
           }
@@ -385,6 +397,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   cluster_sync();  // no remote arrive / MMA of the pair still targets this CTA
+  if (w.span && threadIdx.x == 0) atomicMax(&w.span[1], mt_globaltimer());
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -411,7 +424,7 @@ int g_sm2 = 0;
 // launch over the off-band slot range [s0, s0 + scnt) of step k; `ctas` caps
 // the grid (rounded down to pairs)
 int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
-                  int presplit, cudaStream_t st) {
+                  int presplit, cudaStream_t st, unsigned long long* span, int jlo, int jhi) {
   if (scnt <= 0) return MT_OK;
   CUtensorMap ma, mb;
   const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
@@ -424,6 +437,10 @@ int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   w.nsubn = g.nb / BN;
   w.nitems = (int)(scnt * w.nsubm * w.nsubn);
   w.presplit = presplit;
+  w.span = span;
+  w.mlo = g.owned_before(jlo);
+  w.mhi = g.owned_before(jhi);
+  w.sw = (!trsm && jhi > jlo + 1) ? mt_opt_super_cols() : 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_sm2) cudaDeviceGetAttribute(&g_sm2, cudaDevAttrMultiProcessorCount, dev);

@@ -80,55 +80,6 @@ struct Work {
   int diag;      // diagnostics only (option 8): 1 skip C loads, 2 skip C stores, 4 skip epilogue
 };
 
-// ---- L2-friendly output order of the trailing update -----------------------
-// Slot order (column by column) re-reads every row operand A_ik from HBM once
-// per output column: at p - k = 500 the panel split (2 MB per tile) is far
-// larger than L2.  Instead the outputs are visited in super-columns of `sw`
-// owned columns, rows ascending inside each, columns ascending inside a row:
-// a row operand is then fetched once per super-column and the sw column
-// operands stay L2-resident while the rows sweep past.  Every output tile is
-// still computed by exactly one work item, so results do not depend on it.
-//
-// Owned column m is global column j = c0 + m*cs; its off-band rows are
-// i in [j + t, p).  In a super-column [ma, mb) row i holds the columns
-// m in [ma, min(mb, F(i) + 1)), F(i) = floor((i - t - c0) / cs), so the tiles
-// before row x number P(x) = G(x, ma) - G(x, mb) with
-// G(x, a) = sum_{i<x} max(0, floor((i - d_a) / cs)), d_a = t + c0 + (a - 1) cs,
-// = T(x - d_a) - T(-d_a),  T(Y) = sum_{y<Y} floor(y / cs)  (0 for Y <= 0).
-__device__ __forceinline__ int64_t stair_T(int64_t y, int cs) {
-  if (y <= 0) return 0;
-  const int64_t q = y / cs, r = y % cs;
-  return (int64_t)cs * q * (q - 1) / 2 + r * q;
-}
-__device__ __forceinline__ int64_t stair_G(const Grid& g, int64_t x, int a) {
-  const int64_t d = (int64_t)g.t + g.c0 + (int64_t)(a - 1) * g.cs;
-  return stair_T(x - d, g.cs) - stair_T(-d, g.cs);
-}
-__device__ __forceinline__ int64_t super_prefix(const Grid& g, int64_t x, int ma, int mb) {
-  return stair_G(g, x, ma) - stair_G(g, x, mb);
-}
-// tile index -> (i, j) in super-column order over owned columns [mlo, mhi)
-__device__ void super_tile_ij(const Grid& g, int64_t idx, int mlo, int mhi, int sw, int& i,
-                              int& j) {
-  int ma = mlo;
-  for (;;) {
-    const int mb = min(mhi, ma + sw);
-    const int64_t cnt = super_prefix(g, g.p, ma, mb);
-    if (idx < cnt || mb >= mhi) {
-      int lo = 0, hi = g.p;  // largest row x with P(x) <= idx
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (super_prefix(g, mid, ma, mb) <= idx) lo = mid; else hi = mid;
-      }
-      i = lo;
-      j = g.owned_col(ma + (int)(idx - super_prefix(g, lo, ma, mb)));
-      return;
-    }
-    idx -= cnt;
-    ma = mb;
-  }
-}
-
 constexpr int SCHED = 4;  // work-item ring between the producer and the consumers
 
 // TRSM = false: C_ij -= A_ik A_jk^T (trailing update of step k)
@@ -481,12 +432,11 @@ bool mt_tc_trsm_enabled(const Grid& g) {
 namespace {
 // persistent launch over `nitems` work items of slot range [s0, s0 + scnt)
 int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
-                cudaStream_t st, int jlo = 0, int jhi = 0) {
+                cudaStream_t st, int jlo = 0, int jhi = 0, unsigned long long* span = nullptr) {
   if (scnt <= 0) return MT_OK;
-  if (mt_opt_cta_pairs() && !mt_opt_tc_diag() && !mt_opt_c_prefetch() &&
-      (trsm || mt_opt_super_cols() == 0))  // CTA-pair kernel (tc2_update.cu): slot order only
+  if (mt_opt_cta_pairs() && !mt_opt_tc_diag() && !mt_opt_c_prefetch())  // CTA-pair kernel
     return mt_tc2_launch(g, k, s0, scnt, ctas, trsm,
-                         (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st);
+                         (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st, span, jlo, jhi);
   CUtensorMap ma, mb;
   const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;  // whole split buffer
   int rc = make_map(&ma, g.split, split_rows, g.nb, BM);
@@ -534,9 +484,10 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
 }  // namespace
 
 // FP32 updates of step k into off-band slots [s0, s0+scnt) via tcgen05; `ctas` caps the grid.
-int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st) {
+int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st,
+                      unsigned long long* span) {
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
-  return launch_tc32(g, k, s0, scnt, ctas, false, st, jlo, jhi);
+  return launch_tc32(g, k, s0, scnt, ctas, false, st, jlo, jhi, span);
 }
 
 // Off-band panel TRSM of step k: X_ik = B_ik W^T for the off-band rows of

@@ -421,15 +421,18 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const double a = f64 / 32e12, b = f32 / 215e12;  // seconds on the whole GPU
-    int x = (int)(0.9 * sms * a / (a + b));          // SMs left to the band update
+    int x = (int)(0.01 * mt_opt_coschedule_pct() * sms * a / (a + b));  // SMs left to the band update
+    if (x > sms - 2) x = sms - 2;
     int tc_ctas = (sms - x) & ~1;
     if (tc_ctas < 2) tc_ctas = 2;
-    // one profiling span for the pair (an event between the two launches would
-    // serialise them): kind upd32, flops of both
-    ProfScope ps(MT_K_UPD32, st, f32 + f64,
-                 co_scnt * (double)nb * nb * 4.0 * 2.0 + co_bcnt * (double)nb * nb * 8.0 * 3.0, 2);
-    RC_UPD(mt_tc_update_impl(g, k, jlo, jhi, tc_ctas, st));
-    return mt_dmma_update_impl(g, k, co_b0, co_bcnt, st, true);
+    // no stream events between the two launches (they would serialise them):
+    // both kernels stamp device-side spans for the profiler
+    mt_count_launch(2);
+    unsigned long long* s32 = mt_prof_dspan(MT_K_UPD32, f32, co_scnt * (double)nb * nb * 4.0 * 2.0,
+                                            (double)tc_ctas / sms);
+    unsigned long long* s64 = mt_prof_dspan(MT_K_UPD64, f64, co_bcnt * (double)nb * nb * 8.0 * 3.0);
+    RC_UPD(mt_tc_update_impl(g, k, jlo, jhi, tc_ctas, st, s32));
+    return mt_dmma_update_impl(g, k, co_b0, co_bcnt, st, true, s64);
   }
   // band (FP64) outputs in columns [jlo, jhi)
   const int64_t b0 = g.bcol(jlo), bcnt = g.bcol(jhi) - b0;
