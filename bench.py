@@ -343,13 +343,18 @@ def run_ours(args, rank, world, local_rank):
         "avg_sm_share": sm_share,
         "achieved_on_its_sms_only_raw": achieved_raw,
         "algorithmic_flops_per_launch": d["flops"] / max(1, d["launches"]),
+        "algorithmic_bytes_per_launch": d["bytes"] / max(1, d["launches"]),
         "measured": ("device-side %globaltimer span of every bulk trailing-update launch inside "
                      "the timed region (it runs concurrently with the co-scheduled FP64 band "
                      "update on the same stream, so stream events cannot bracket it), weighted "
                      "by the share of SMs the launch was given; algorithmic flops = reference "
                      "flop model (factor.py:83-95) per launch"),
         "share_of_step": d["ms"] / (t_dev / args.steps * 1e3),
-        "traffic_source": "profiles/ncu_traffic.json (ncu dram__bytes_read+write per launch)",
+        "traffic_source": ("profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk launch "
+                           "(grid 296) of the bench command; above the algorithmic C read+write "
+                           "because the A-panel rows are re-fetched per output column (the panel, "
+                           "2 MB/tile, exceeds L2); the kernel is tensor-bound at ~54% of HBM "
+                           "bandwidth (DESIGN.md section 4)"),
         "cholesky_flop_weighted": {
             "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
             "f_sp": fl_plan.sp, "f_dp": fl_plan.dp,

@@ -37,7 +37,13 @@ using namespace mt_tma;
 constexpr int BM = 128;               // accumulator rows per CTA (pair M = 256)
 constexpr int BN = 256;               // pair N; each CTA stages BN / 2 rows of B
 constexpr int BNH = BN / 2;
-constexpr int BK = 16, STAGES = 6;
+#ifndef MT_TC2_TMAEPI
+#define MT_TC2_TMAEPI 1
+#endif
+// MT_TC2_TMAEPI: the bulk update's epilogue streams C through shared memory
+// with TMA (4 x 4 KB SWIZZLE_128B chunk slots per warp, loads issued up to 3
+// chunks ahead, results stored back by TMA); 5 operand stages leave room for it
+constexpr int BK = 16, STAGES = MT_TC2_TMAEPI ? 5 : 6;
 constexpr int A_BYTES = BM * BK * 4;  // 8 KB
 constexpr int B_BYTES = BNH * BK * 4; // 8 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
@@ -50,10 +56,13 @@ constexpr int EPI_WARPS = MT_TC2_EPI;
 constexpr int EPI_COLS = BN / (EPI_WARPS / 4);
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int EPI_STRIDE = 33;
-constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_STRIDE * 4;
+constexpr int CSLOTS = 4, CSLOT_BYTES = 32 * 32 * 4;  // TMA epilogue: per-warp C chunk ring
+constexpr int EPI_BYTES = MT_TC2_TMAEPI ? EPI_WARPS * CSLOTS * CSLOT_BYTES
+                                        : EPI_WARPS * 32 * EPI_STRIDE * 4;
+static_assert(!MT_TC2_TMAEPI || EPI_WARPS == 4, "TMA epilogue assumes one warp per TMEM quadrant");
 constexpr int TMEM_COLS = 512;        // 2 accumulators x 256 columns
 constexpr int SCHED = 4;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 512;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 640;
 
 __device__ __forceinline__ uint64_t sw64_desc(const void* p) {
   const uint64_t a = (smem_u32(p) >> 4) & 0x3FFF;
@@ -109,6 +118,35 @@ __device__ __forceinline__ void tma_load_pair(void* dst, const CUtensorMap* map,
       "l"((uint64_t)map), "r"(bar_cl), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          (uint64_t)map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void umma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -136,7 +174,8 @@ struct Work2 {
 
 template <bool TRSM>
 __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
-                                         const CUtensorMap& map_a, const CUtensorMap& map_b) {
+                                         const CUtensorMap& map_a, const CUtensorMap& map_b,
+                                         const CUtensorMap& map_c) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   float* epi = (float*)(smem + STAGES * STAGE_BYTES);
@@ -149,7 +188,8 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
   int* sitem = (int*)(sempty + SCHED);
   int* si = sitem + SCHED;  // tile row i of the item
   int* sj = si + SCHED;     // tile column j of the item
-  uint32_t* tmem_slot = (uint32_t*)(sj + SCHED);
+  uint64_t* cbar = (uint64_t*)(sj + SCHED);  // TMA epilogue: C chunk slots, CSLOTS per warp
+  uint32_t* tmem_slot = (uint32_t*)(cbar + EPI_WARPS * CSLOTS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // co-scheduled band update (option 10): once every pair of this grid is
@@ -176,6 +216,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       mbar_init(&sfull[s], 1);
       mbar_init(&sempty[s], 2 + 2 * EPI_WARPS);  // leader: MMA + epi + peer producer + peer epi
     }
+    for (int s = 0; s < EPI_WARPS * CSLOTS; ++s) mbar_init(&cbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -317,9 +358,16 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
   } else {
     // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
     const int c_lo = EPI_WARPS == 4 ? 0 : ((warp - 2) / 4) * EPI_COLS;  // this warp's columns
     const uint32_t tempty_leader[2] = {peer_addr(&tempty[0], 0), peer_addr(&tempty[1], 0)};
+#if MT_TC2_TMAEPI
+    unsigned char* wslots = (unsigned char*)epi + (warp - 2) * CSLOTS * CSLOT_BYTES;
+    uint64_t* wbar = cbar + (warp - 2) * CSLOTS;
+    float* stg = (float*)wslots;  // register-path transpose buffer aliases the slots
+    uint32_t gl = 0, gu = 0;      // C chunks loaded / used by this warp (slot = n % CSLOTS)
+#else
+    float* stg = epi + (warp - 2) * 32 * EPI_STRIDE;
+#endif
     for (uint32_t li = 0;; ++li) {
       int i, j;
       const int item = next_item(li, &i, &j);
@@ -329,6 +377,73 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       const uint32_t b = li & 1, aph = (li >> 1) & 1;
       const int64_t roff = (int64_t)(m0 + q * 32) * nb + n0;
       float* cbase = g.stile(i, j) + roff;
+#if MT_TC2_TMAEPI
+      if (!TRSM && !(w.presplit && j == k + 1)) {
+        // ---- TMA path: C chunk (32 rows x 32 columns, SWIZZLE_128B) per slot;
+        // lane = row, matching the tcgen05.ld 32x32b layout (no transpose)
+        const int crow = (int)((g.scol(j) + (i - j - g.t)) * (int64_t)nb) + m0 + q * 32;
+        auto load_chunk = [&](int c, int newer) {  // newer: stores issued after the slot's last one
+          if (lane == 0) {
+            if (newer >= 3) bulk_wait_read<3>();
+            else if (newer == 2) bulk_wait_read<2>();
+            else if (newer == 1) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+            const uint32_t s = gl % CSLOTS;
+            mbar_expect_tx(&wbar[s], CSLOT_BYTES);
+            tma_load_2d(wslots + s * CSLOT_BYTES, &map_c, &wbar[s], n0 + c * 32, crow);
+          }
+          ++gl;
+        };
+        for (int c = 0; c < 3; ++c) load_chunk(c, (int)gu - (int)gl + 3);
+        mbar_wait(&tfull[b], aph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+              "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+                "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+                "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+                "=r"(v[31])
+              : "r"(taddr + c * 32));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const uint32_t s = gu % CSLOTS;
+          mbar_wait(&wbar[s], (gu / CSLOTS) & 1);
+          const uint32_t row = smem_u32(wslots + s * CSLOT_BYTES) + lane * 128;
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            const uint32_t a = row + ((x ^ (lane & 7)) << 4);
+            float4 cc = lds128(a);
+            cc.x -= __uint_as_float(v[4 * x]);
+            cc.y -= __uint_as_float(v[4 * x + 1]);
+            cc.z -= __uint_as_float(v[4 * x + 2]);
+            cc.w -= __uint_as_float(v[4 * x + 3]);
+            sts128(a, cc);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, wslots + s * CSLOT_BYTES, n0 + c * 32, crow);
+            bulk_commit();
+          }
+          ++gu;
+          if (c + 3 < BN / 32) load_chunk(c + 3, (int)gu - (int)gl + 3);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl_relaxed(tempty_leader[b]);
+        continue;
+      }
+      // register path (TRSM, or the column-(k+1) update with its split outputs):
+      // its transpose buffer aliases the chunk slots -> drain the TMA stores first
+      if (lane == 0) bulk_wait_all();
+      __syncwarp();
+#endif
       float cn[32];
       if constexpr (!TRSM) {
 #pragma unroll
@@ -392,7 +507,15 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       __syncwarp();
       // TMEM reads completed (tcgen05.wait::ld): relaxed arrive, no wait on the C stores
       if (lane == 0) mbar_arrive_cl_relaxed(tempty_leader[b]);
+#if MT_TC2_TMAEPI
+      // the transpose buffer's generic writes precede later TMA refills of the slots
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     }
+#if MT_TC2_TMAEPI
+    if (lane == 0) bulk_wait_all();  // C stores complete before the kernel ends
+    __syncwarp();
+#endif
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -407,14 +530,16 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tc2_update_kernel(Grid g, int k, Work2 w, const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b) {
-  tc2_body<false>(g, k, w, map_a, map_b);
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_c) {
+  tc2_body<false>(g, k, w, map_a, map_b, map_c);
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tc2_trsm_kernel(Grid g, int k, Work2 w, const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b) {
-  tc2_body<true>(g, k, w, map_a, map_b);
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c) {
+  tc2_body<true>(g, k, w, map_a, map_b, map_c);
 }
 
 int g_sm2 = 0;
@@ -430,6 +555,11 @@ int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
   int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
+  // C (off-band pool) in 32 x 32 FP32 chunks for the TMA epilogue
+  CUtensorMap mc;
+  const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;
+  if (!rc) rc = make_map_2d(&mc, g.sp ? (const void*)g.sp : (const void*)g.split, c_rows, g.nb, 4, 32,
+                            32, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   Work2 w;
   w.slot0 = s0;
@@ -459,11 +589,11 @@ int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   const size_t smem = SMEM_BYTES;
   if (trsm) {
     cudaFuncSetAttribute(tc2_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tc2_trsm_kernel<<<2 * pairs, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+    tc2_trsm_kernel<<<2 * pairs, NUM_THREADS, smem, st>>>(g, k, w, ma, mb, mc);
     MT_LAUNCH_CHECK("tc2_trsm_kernel");
   } else {
     cudaFuncSetAttribute(tc2_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tc2_update_kernel<<<2 * pairs, NUM_THREADS, smem, st>>>(g, k, w, ma, mb);
+    tc2_update_kernel<<<2 * pairs, NUM_THREADS, smem, st>>>(g, k, w, ma, mb, mc);
     MT_LAUNCH_CHECK("tc2_update_kernel");
   }
   return MT_OK;

@@ -12,6 +12,11 @@ ap.add_argument("--dp", action="store_true")
 ap.add_argument("--warm", type=int, default=1)
 ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
+if os.environ.get("MT_OPTS"):  # e.g. MT_OPTS=10=0 (library runtime options)
+    from paper_2003_05324_b200 import _lib
+    for kv in os.environ["MT_OPTS"].split(","):
+        k_, v_ = kv.split("=")
+        _lib.load().mt_set_option(int(k_), int(v_))
 locs = mt.generate_locations(a.n, seed=mt.derive_seed(0, 0))
 ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.random.default_rng(1).standard_normal(a.n)))
 pol = mt.PrecisionPolicy.dp() if a.dp else mt.PrecisionPolicy.mp(diag_thick=a.t)
