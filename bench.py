@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=262144)
+    ap.add_argument("--n", "--matrix-n", dest="n", type=int, default=262144)
     ap.add_argument("--nb", type=int, default=512)
     ap.add_argument("--t", type=int, default=8)
     ap.add_argument("--dp-n", type=int, default=65536,
@@ -232,6 +232,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2003_05324_b200 import _lib
     from paper_2003_05324_b200.distributed import DistributedEvaluator, loglik_distributed
 
+    local_rank = local_rank % torch.cuda.device_count()  # (dev gloo check: ranks share a GPU)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     lib = _lib.load()
@@ -481,12 +482,18 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
+        torch.cuda.set_device(local_rank % torch.cuda.device_count())
         # high-priority NCCL streams: the panel broadcasts get SMs ahead of the
         # bulk update's pending CTAs (which also yield on request)
-        opts = dist.ProcessGroupNCCL.Options()
-        opts.is_high_priority_stream = True
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), pg_options=opts)
+        if os.environ.get("MT_BENCH_BACKEND", "nccl") == "gloo":
+            # dev check of the multi-rank bench logic on a one-GPU box (ranks share cuda:0;
+            # NCCL refuses that); never used for reported numbers
+            dist.init_process_group("gloo")
+        else:
+            opts = dist.ProcessGroupNCCL.Options()
+            opts.is_high_priority_stream = True
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                    pg_options=opts)
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
