@@ -405,7 +405,10 @@ def run_ours(args, rank, world, local_rank):
         dp_bytes = p_tiles * (p_tiles + 1) // 2 * nb * nb * 8 / world
         free_bytes = torch.cuda.mem_get_info()[0]
         free_min = -max_over_ranks(-float(free_bytes)) if dist_on else free_bytes
-        if dp_bytes < 0.9 * free_min:
+        # full DP at the headline N only when it fits and stays short (DMMA ~28 TF/s per
+        # GPU under the power cap): 8 GPUs at N=262144 ~25 s; otherwise configs[1]
+        dp_secs = (n ** 3 / 3.0) / (world * 28e12)
+        if dp_bytes < 0.9 * free_min and dp_secs < 60.0:
             dn, dt, dasm, mp_ref = n, t, asm, value
         else:
             dn, dt = args.dp_n, args.dp_t
@@ -437,8 +440,8 @@ def run_ours(args, rank, world, local_rank):
         dp = {"n": dn, "mp_band_t": dt, "dp_evals_per_s": 1.0 / t_dp, "dp_ms_per_eval": t_dp * 1e3,
               "mp_evals_per_s": mp_ref, "mp_speedup": mp_ref * t_dp,
               "note": ("same N as the headline" if dn == n else
-                       f"full DP at N={n} needs {dp_bytes * world / 1e9:.0f} GB > "
-                       f"{world} GPU(s): compared at configs[1] N={dn}")}
+                       f"full DP at N={n} needs {dp_bytes * world / 1e9:.0f} GB and ~{dp_secs:.0f} s "
+                       f"on {world} GPU(s): compared at configs[1] N={dn}")}
         del evd
         _free_memory()
 

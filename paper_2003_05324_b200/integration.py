@@ -41,6 +41,17 @@ def _targets(pkg):
         out.append((pm, {"cholesky": F.cholesky, "solve": F.solve,
                          "assemble_covariance": T.assemble_covariance, "krige": P.krige}))
     out.append((pkg, {"krige": P.krige}))
+    # the reference CLI (cli.py:21-42) binds its own names: `mixtile bench`,
+    # `estimate` and `predict` then run on the device too (cmd_bench,
+    # cli.py:225-271: assemble -> cholesky -> logdet -> solve, residual vs DP)
+    try:
+        cm = mod("cli")
+    except ImportError:
+        cm = None
+    if cm is not None:
+        out.append((cm, {"TileAssembler": T.TileAssembler, "cholesky": F.cholesky,
+                         "factor_logdet": F.logdet, "factor_solve": F.solve,
+                         "reconstruction_error": F.reconstruction_error}))
     return out, f, t
 
 

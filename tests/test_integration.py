@@ -33,6 +33,10 @@ def test_install_rebinds_consumers(mixtile):
         assert mixtile.mle.TileAssembler is mt.TileAssembler
         assert mixtile.tilestore.assemble_covariance is mt.assemble_covariance
         assert mixtile.predict.cholesky is mt.cholesky
+        assert mixtile.predict.krige is mt.krige
+        # the reference CLI's bench/estimate/predict commands follow
+        assert mixtile.cli.cholesky is mt.cholesky and mixtile.cli.TileAssembler is mt.TileAssembler
+        assert mixtile.cli.factor_logdet is mt.logdet and mixtile.cli.factor_solve is mt.solve
         # the GPU path raises the reference's exception types
         assert F.FactorizationError is mixtile.factor.FactorizationError
         assert ("mixtile.mle", "cholesky") in rebound
