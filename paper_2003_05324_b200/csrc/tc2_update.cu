@@ -35,7 +35,17 @@ namespace {
 using namespace mt_tma;
 
 constexpr int BM = 128;               // accumulator rows per CTA (pair M = 256)
-constexpr int BN = 256;               // pair N; each CTA stages BN / 2 rows of B
+#ifndef MT_TC2_SPLITACC
+#define MT_TC2_SPLITACC 0
+#endif
+// MT_TC2_SPLITACC: accumulate the hi*hi products and the two correction
+// products (lo*hi, hi*lo) in separate TMEM accumulators, summed in FP32 by the
+// epilogue.  The tensor core adds each K=8 partial into TMEM with
+// round-toward-zero; keeping the small correction terms out of the large
+// accumulator removes 2/3 of those biased additions at full magnitude
+// (tools/emulate_tf32x3.py).  Costs N = 128 items (TMEM holds 2 x 2 x 128).
+constexpr int BN = MT_TC2_SPLITACC ? 128 : 256;  // pair N; each CTA stages BN / 2 rows of B
+constexpr int ACC_STRIDE = MT_TC2_SPLITACC ? 2 * BN : BN;  // TMEM columns per accumulator buffer
 constexpr int BNH = BN / 2;
 #ifndef MT_TC2_TMAEPI
 #define MT_TC2_TMAEPI 1
@@ -43,10 +53,10 @@ constexpr int BNH = BN / 2;
 // MT_TC2_TMAEPI: the bulk update's epilogue streams C through shared memory
 // with TMA (4 x 4 KB SWIZZLE_128B chunk slots per warp, loads issued up to 3
 // chunks ahead, results stored back by TMA); 5 operand stages leave room for it
-constexpr int BK = 16, STAGES = MT_TC2_TMAEPI ? 5 : 6;
+constexpr int BK = 16, STAGES = MT_TC2_SPLITACC ? 6 : (MT_TC2_TMAEPI ? 5 : 6);
 constexpr int A_BYTES = BM * BK * 4;  // 8 KB
-constexpr int B_BYTES = BNH * BK * 4; // 8 KB
-constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
+constexpr int B_BYTES = BNH * BK * 4; // 8 KB (4 KB with split accumulators)
+constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB (24 KB split)
 #ifndef MT_TC2_EPI
 #define MT_TC2_EPI 4
 #endif
@@ -146,6 +156,22 @@ __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
                : "memory");
+}
+// v[u] += (correction accumulator, 32 columns at taddr) in FP32 round-to-nearest
+__device__ __forceinline__ void add_corr(uint32_t (&v)[32], uint32_t taddr) {
+  uint32_t w[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+        "=r"(w[14]), "=r"(w[15]), "=r"(w[16]), "=r"(w[17]), "=r"(w[18]), "=r"(w[19]), "=r"(w[20]),
+        "=r"(w[21]), "=r"(w[22]), "=r"(w[23]), "=r"(w[24]), "=r"(w[25]), "=r"(w[26]), "=r"(w[27]),
+        "=r"(w[28]), "=r"(w[29]), "=r"(w[30]), "=r"(w[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int u = 0; u < 32; ++u) v[u] = __float_as_uint(__uint_as_float(v[u]) + __uint_as_float(w[u]));
 }
 __device__ __forceinline__ void umma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
@@ -328,7 +354,8 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
         const uint32_t b = li & 1, aph = (li >> 1) & 1;
         mbar_wait_cl(&tempty[b], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t dcol = tmem_base + b * BN;
+        const uint32_t dcol = tmem_base + b * ACC_STRIDE;
+        const uint32_t ccol = MT_TC2_SPLITACC ? dcol + BN : dcol;  // correction accumulator
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -344,9 +371,10 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
             for (int kk = 0; kk < BK / 8; ++kk) {
               const int off = kk * 32;  // 8 fp32 along K = 32 B inside the 64 B swizzle row
               const uint32_t first = (ks == 0 && kk == 0) ? 0u : 1u;
-              umma2_tf32(dcol, sw64_desc(alo + off), sw64_desc(bhi + off), first);
-              umma2_tf32(dcol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
-              umma2_tf32(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off), 1u);
+              umma2_tf32(ccol, sw64_desc(alo + off), sw64_desc(bhi + off), first);
+              umma2_tf32(ccol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
+              umma2_tf32(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off),
+                         MT_TC2_SPLITACC ? first : 1u);
             }
             umma2_commit_both(&empty[s]);                        // both CTAs' stage s free
             if (ks == ksteps - 1) umma2_commit_both(&tfull[b]);  // both accumulators ready
@@ -397,7 +425,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
         for (int c = 0; c < 3; ++c) load_chunk(c, (int)gu - (int)gl + 3);
         mbar_wait(&tfull[b], aph);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * ACC_STRIDE;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t v[32];
@@ -412,6 +440,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
                 "=r"(v[31])
               : "r"(taddr + c * 32));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (MT_TC2_SPLITACC) add_corr(v, taddr + BN + c * 32);
           const uint32_t s = gu % CSLOTS;
           mbar_wait(&wbar[s], (gu / CSLOTS) & 1);
           const uint32_t row = smem_u32(wslots + s * CSLOT_BYTES) + lane * 128;
@@ -454,7 +483,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
       float* shi = TRSM ? g.split_hi(i, k) + roff
                         : ((w.presplit && j == k + 1) ? g.presplit_hi(i) + roff : nullptr);
       const int64_t te = g.tile_elems();
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + b * ACC_STRIDE;
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + EPI_COLS; c += 32) {
         uint32_t v[32];
@@ -469,6 +498,7 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
               "=r"(v[31])
             : "r"(taddr + c));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (MT_TC2_SPLITACC) add_corr(v, taddr + BN + c);
 #pragma unroll
         for (int u = 0; u < 32; ++u) stg[lane * EPI_STRIDE + u] = __uint_as_float(v[u]);
         __syncwarp();
