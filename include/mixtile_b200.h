@@ -137,6 +137,13 @@ int mt_cross_gemv(const double* test, int64_t m, const double* train, int64_t n,
  * sets status[0] to the global 0-based index (FactorizationError.index). */
 int mt_cholesky(const mt_tiles* g, int32_t lookahead, void* stream);
 
+/* mt_cholesky with the forward sweep of mt_quad fused into the schedule (each
+ * column's TRSV/GEMV step issued as soon as the column is final, underneath the
+ * bulk updates): factors in place and writes quad = ||L^{-1} z||^2 to *out
+ * (device), bitwise equal to mt_cholesky + mt_quad.  work: mt_work_doubles(). */
+int mt_cholesky_quad(const mt_tiles* g, int32_t lookahead, const double* z, double* work,
+                     double* out, void* stream);
+
 /* Device scratch (doubles) needed by mt_logdet / mt_quad / mt_evaluate:
  * p*nb + 2048 + p. */
 int64_t mt_work_doubles(const mt_tiles* g);

@@ -76,6 +76,7 @@ SIGNATURES = {
     "mt_cross_work_doubles": (_I64, [_I64, _I64]),
     "mt_cross_gemv": (ctypes.c_int, [_V, _I64, _V, _I64, _I32, _D, _P(MtMatern), _V, _V, _V, _V]),
     "mt_cholesky": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
+    "mt_cholesky_quad": (ctypes.c_int, [_P(MtTiles), _I32, _V, _V, _V, _V]),
     "mt_logdet": (ctypes.c_int, [_P(MtTiles), _V, _V, _V]),
     "mt_solve": (ctypes.c_int, [_P(MtTiles), _V, _I64, _I32, _V]),
     "mt_quad": (ctypes.c_int, [_P(MtTiles), _V, _V, _V, _V]),

@@ -135,16 +135,21 @@ DevCtx* dev_ctx() {
 }  // namespace
 
 // ------------------------------------------------------------------ the DAG
-static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main) {
+// fwd (optional): a device vector (zero-padded, p*nb) on which the forward
+// sweep y = L^{-1} x runs fused into the schedule: column k's step (the same
+// TRSV + GEMV kernels as mt_solve's forward sweep, so results are identical)
+// is issued right after panel k is final, underneath the bulk updates.
+static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main,
+                             double* fwd = nullptr) {
   const int p = g.p;
   auto narrow_k = [&](int k) { return (g.mode == MT_MODE_MP && k + g.t <= p - 1) ? 1 : 0; };
+  auto fwd_step = [&](int k, cudaStream_t s) { return fwd ? mt_fwd_step_impl(g, k, fwd, s) : MT_OK; };
   if (!lookahead || p < 3) {
     for (int k = 0; k < p; ++k) {
       RC(mt_potrf_impl(g, k, narrow_k(k), main));
-      if (k + 1 < p) {
-        RC(mt_trsm_impl(g, k, main));
-        RC(mt_update_impl(g, k, k + 1, p, main));
-      }
+      if (k + 1 < p) RC(mt_trsm_impl(g, k, main));
+      RC(fwd_step(k, main));
+      if (k + 1 < p) RC(mt_update_impl(g, k, k + 1, p, main));
     }
     return MT_OK;
   }
@@ -169,6 +174,7 @@ static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main) {
   CK(cudaStreamWaitEvent(pan, e, 0), "stream wait");
   RC(mt_potrf_impl(g, 0, narrow_k(0), pan));
   RC(mt_trsm_impl(g, 0, pan));
+  RC(fwd_step(0, pan));
   for (int k = 0; k < p - 1; ++k) {
     cudaEvent_t ep = ctx->event();
     CK(cudaEventRecord(ep, pan), "event record");   // panel k ready
@@ -183,6 +189,7 @@ static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main) {
       RC(mt_trsm_impl(g, k + 1, pan, yield_on ? &ask : nullptr));
       RC(request(0u));
     }
+    RC(fwd_step(k + 1, pan));  // panel k+1 is final
     // caller stream: the rest of step k's trailing update
     RC(mt_update_impl(gb, k, k + 2, p, main));
     cudaEvent_t em = ctx->event();
@@ -377,6 +384,19 @@ int mt_cross_gemv(const double* test, int64_t m, const double* train, int64_t n,
                             (cudaStream_t)stream);
 }
 
+int mt_cholesky_quad(const mt_tiles* t, int32_t lookahead, const double* z, double* work,
+                     double* out, void* stream) {
+  RC(check_layout(t));
+  RC(single_gpu_only(t, "mt_cholesky_quad"));
+  if (!z || !work || !out) { mt_set_error("mt_cholesky_quad: null argument"); return MT_E_BAD_ARG; }
+  const Grid g = make_grid(t);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t npad = (int64_t)g.p * g.nb;
+  CK(cudaMemcpyAsync(work, z, npad * sizeof(double), cudaMemcpyDeviceToDevice, st), "quad copy");
+  RC(cholesky_schedule(g, lookahead, st, work));
+  return mt_sumsq_impl(work, npad, work + npad, out, st);
+}
+
 int mt_cholesky(const mt_tiles* t, int32_t lookahead, void* stream) {
   RC(check_layout(t));
   RC(single_gpu_only(t, "mt_cholesky"));
@@ -509,10 +529,12 @@ int mt_evaluate(const mt_tiles* t, const double* locs, int32_t metric, double ra
   const Grid g = make_grid(t);
   cudaStream_t st = (cudaStream_t)stream;
   RC(mt_generate_impl(g, locs, metric, radius, *theta, st));
-  RC(cholesky_schedule(g, lookahead, st));
+  // quad = ||L^{-1} z||^2 with the forward sweep fused into the factorization
   const int64_t npad = (int64_t)g.p * g.nb;
+  CK(cudaMemcpyAsync(work, z, npad * sizeof(double), cudaMemcpyDeviceToDevice, st), "quad copy");
+  RC(cholesky_schedule(g, lookahead, st, work));
   RC(mt_logdet_impl(g, out2, work + npad + 2048, st));
-  RC(mt_quad_impl(g, z, work, out2 + 1, st));
+  RC(mt_sumsq_impl(work, npad, work + npad, out2 + 1, st));
   return MT_OK;
 }
 

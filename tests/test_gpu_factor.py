@@ -242,3 +242,35 @@ def test_large_tile_factor_vs_oracle(gpu):
         np.testing.assert_allclose(f.tiles[key].dp, dp, rtol=0, atol=1e-11, err_msg=str(key))
     assert math.isclose(mt.logdet(f), O.logdet(ref, 4), rel_tol=1e-11)
     np.testing.assert_allclose(mt.solve(f, ds.z), O.solve(ref, n, nb, ds.z), rtol=1e-8, atol=1e-8)
+
+
+@pytest.mark.parametrize("n,nb,t,la", [(3000, 256, 2, 1), (4096, 512, 8, 1), (1500, 256, 6, 0)])
+def test_fused_forward_sweep_bitwise(gpu, n, nb, t, la):
+    """mt_cholesky_quad (forward sweep fused into the factorization schedule)
+    equals mt_cholesky followed by mt_quad bit for bit: same kernels per column,
+    issued as soon as the column is final."""
+    import ctypes
+    import torch
+    mt = _mt()
+    from paper_2003_05324_b200 import _lib
+    lib, st = _lib.load(), _lib.stream_handle()
+    locs = mt.generate_locations(n, seed=41)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.random.default_rng(42).standard_normal(n)))
+    asm = mt.TileAssembler(ds, nb)
+    pol = mt.PrecisionPolicy.mp(diag_thick=t)
+    outs = []
+    for fused in (0, 1):
+        m = mt.TileMatrix(n, nb, pol)
+        asm.generate_into(m, mt.MaternParams(1.0, 0.1, 0.5))
+        d = ctypes.byref(m.desc)
+        work = torch.zeros(lib.mt_work_doubles(d), dtype=torch.float64, device=m.device)
+        out = torch.zeros(1, dtype=torch.float64, device=m.device)
+        if fused:
+            _lib.check(lib.mt_cholesky_quad(d, la, _lib.ptr(asm.d_z), _lib.ptr(work), _lib.ptr(out),
+                                            st), "mt_cholesky_quad")
+        else:
+            _lib.check(lib.mt_cholesky(d, la, st), "mt_cholesky")
+            _lib.check(lib.mt_quad(d, _lib.ptr(asm.d_z), _lib.ptr(work), _lib.ptr(out), st), "mt_quad")
+        torch.cuda.synchronize()
+        outs.append(float(out.item()))
+    assert outs[0] == outs[1]
