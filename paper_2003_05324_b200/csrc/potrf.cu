@@ -3,8 +3,8 @@
 //
 // One CTA (8 warps) walks the tile in 32-wide column blocks, right-looking:
 //   1. warp 0 factors the 32x32 diagonal block with the rows held in
-//      registers (lane r owns row r, pivots broadcast by shuffles), then
-//      forms its triangular inverse (lane c owns column c);
+//      registers (lane r owns row r, pivots broadcast by shuffles, no CTA
+//      barrier per pivot), then the CTA forms its triangular inverse;
 //   2. the sub-diagonal panel is solved as a parallel GEMM against that
 //      inverse (X = A L_dd^{-T}), staged in shared memory;
 //   3. the trailing lower triangle takes the rank-32 SYRK update on the FP64
@@ -43,41 +43,39 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int n
 
   for (int c0 = 0, blk = 0; c0 < nb; c0 += 32, ++blk) {
     const int w = min(32, nb - c0);
-    // ---------------- 1. diagonal block: factor + inverse (warp 0) --------
-    // (compact loops, not unrolled: this runs once per block on one warp and
-    //  a fully unrolled version blows the instruction cache)
-    for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
-      const int r = e >> 5, c = e & 31;
-      Ld[r][c] = (r < w && c < w) ? (c <= r ? A[(int64_t)(c0 + r) * nb + c0 + c] : 0.0)
-                                  : (r == c ? 1.0 : 0.0);
-    }
-    __syncthreads();
-    // right-looking, one pivot per step, the whole CTA on each step
+    // ---------------- 1. diagonal block: factor (warp 0) + inverse (CTA) --
+    // Warp 0 factors the block with lane r holding row r in registers: the 32
+    // dependent pivot steps use shuffles and __syncwarp-free register updates
+    // instead of three CTA barriers each.  a[cc] is column j + cc of the row
+    // (the window shifts left after every pivot, so indices stay static).
+    if (warp == 0) {
+      const int r = lane;
+      double a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        a[c] = (r < w && c < w) ? (c <= r ? A[(int64_t)(c0 + r) * nb + c0 + c] : 0.0)
+                                : (r == c ? 1.0 : 0.0);
+      int fail = -1;
 #pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-      const double piv = Ld[j][j];
-      if (!(piv > 0.0)) {  // uniform: every thread reads the same pivot
-        if (threadIdx.x == 0) bad = c0 + j;
-        break;
+      for (int j = 0; j < 32; ++j) {
+        double piv = __shfl_sync(0xffffffffu, a[0], j);
+        if (fail < 0 && !(piv > 0.0)) fail = j;  // warp-uniform; later steps are discarded
+        if (fail >= 0) piv = 1.0;
+        const double d = sqrt(piv);
+        double lrj = a[0];
+        if (r == j) lrj = d;
+        else if (r > j) lrj = lrj / d;
+        Ld[r][j] = r >= j ? lrj : 0.0;
+#pragma unroll
+        for (int cc = 1; cc < 32; ++cc) {
+          const double lcj = __shfl_sync(0xffffffffu, lrj, (j + cc) & 31);  // L[j+cc][j]
+          if (j + cc < 32 && r >= j + cc) a[cc] -= lrj * lcj;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 31; ++cc) a[cc] = a[cc + 1];
+        a[31] = 0.0;
       }
-      const double d = sqrt(piv);
-      __syncthreads();  // everyone has read the pivot
-      if (threadIdx.x < 32) {
-        const int r = threadIdx.x;
-        if (r > j) Ld[r][j] = Ld[r][j] / d;
-        else if (r == j) Ld[j][j] = d;
-      }
-      __syncthreads();
-      // rank-1 update of the trailing (r >= c > j) part: one element per thread slot
-      const int jj = 31 - j;  // trailing order
-      for (int e = threadIdx.x; e < jj * (jj + 1) / 2; e += kThreads) {
-        int rr = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-        while (rr * (rr + 1) / 2 > e) --rr;
-        while ((rr + 1) * (rr + 2) / 2 <= e) ++rr;
-        const int r = j + 1 + rr, c = j + 1 + (e - rr * (rr + 1) / 2);
-        Ld[r][c] -= Ld[r][j] * Ld[c][j];
-      }
-      __syncthreads();
+      if (fail >= 0 && lane == 0) bad = c0 + fail;
     }
     __syncthreads();
     if (bad < 0) {
