@@ -434,6 +434,10 @@ namespace {
 int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
                 cudaStream_t st, int jlo = 0, int jhi = 0, unsigned long long* span = nullptr) {
   if (scnt <= 0) return MT_OK;
+  // full-width (256 x 512) CTA-pair items for the bulk update (tc2w_update.cu)
+  if (!trsm && mt_opt_wide_items() && mt_opt_cta_pairs() && mt_tc2w_supported(g) && jlo > k + 1 &&
+      !mt_opt_tc_diag() && !mt_opt_c_prefetch() && mt_opt_super_cols() == 0)
+    return mt_tc2w_launch(g, k, s0, scnt, ctas, st, span);
   if (mt_opt_cta_pairs() && !mt_opt_tc_diag() && !mt_opt_c_prefetch())  // CTA-pair kernel
     return mt_tc2_launch(g, k, s0, scnt, ctas, trsm,
                          (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st, span, jlo, jhi);

@@ -237,3 +237,30 @@ def test_coscheduled_band_update_bitwise(gpu, n, nb, t):
             lib.mt_set_option(10, old)
     for key in facs[0].tiles:
         assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
+
+
+@pytest.mark.parametrize("n,t,co", [(8192, 3, 1), (7000, 2, 0), (12288, 8, 1)])
+def test_wide_pair_items_bitwise(gpu, n, t, co):
+    """Option 12 (bulk update on 256 x 512 CTA-pair items, single-buffered TMEM)
+    applies the same MMA sequence per output element: bitwise equal to the
+    256 x 256-item kernel, with and without co-scheduling, ragged last tile."""
+    mt = _mt()
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    locs = mt.generate_locations(n, seed=31)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    pol = mt.PrecisionPolicy.mp(diag_thick=t)
+    facs = []
+    oc = lib.mt_set_option(10, co)
+    try:
+        for wide in (0, 1):
+            old = lib.mt_set_option(12, wide)
+            try:
+                facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5),
+                                                               512, pol), lookahead=1))
+            finally:
+                lib.mt_set_option(12, old)
+    finally:
+        lib.mt_set_option(10, oc)
+    for key in facs[0].tiles:
+        assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
