@@ -267,7 +267,8 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *      SMs a capped bulk FP32 update leaves free (default), 0 = one after the other
  *  11: band update's SM share under option 10, in % of its work share (default 90)
  *  12: 1 = bulk FP32 update on full-width 256 x 512 CTA-pair items (two N=256 MMAs
- *      per product, single-buffered TMEM; needs nb % 512 == 0), 0 = 256 x 256 items */
+ *      per product, single-buffered TMEM; needs nb % 512 == 0; default), 0 = 256 x 256 items
+ *  13: 1 = the 256 x 512 update prefetches each epilogue warp's C rows into L2 */
 int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */

@@ -238,7 +238,8 @@ static int g_tc_trsm = 1;      // 1 = off-band TRSM as a tcgen05 3xTF32 GEMM aga
 static int g_super_cols = 0;   // super-column width of the bulk FP32 update order (0 = slot order)
 static int g_coschedule = 1;   // 1 = band DMMA update co-scheduled beside the capped FP32 update
 static int g_cosched_pct = 90; // band update's SM share, % of its work share (option 11)
-static int g_wide_items = 0;   // 1 = bulk FP32 update on 256 x 512 pair items (nb % 512 == 0)
+static int g_wide_items = 1;   // 1 = bulk FP32 update on 256 x 512 pair items (nb % 512 == 0)
+static int g_wide_l2pf = 0;    // 1 = the 256 x 512 update stages each warp's C rows in L2
 static int g_cta_pairs = 1;    // 1 = FP32 update/TRSM on CTA pairs (tcgen05 cta_group::2)
 static int g_tc_diag = 0;      // diagnostics (wrong results): 1 no C loads, 2 no C stores, 4 no epilogue
 static int g_c_prefetch = 0;   // 1 = FP32 update stages each item's C block in L2 (cp.async.bulk.prefetch)
@@ -253,6 +254,7 @@ int mt_opt_c_prefetch() { return g_c_prefetch; }
 int mt_opt_tc_diag() { return g_tc_diag; }
 int mt_opt_cta_pairs() { return g_cta_pairs; }
 int mt_opt_wide_items() { return g_wide_items; }
+int mt_opt_wide_l2pf() { return g_wide_l2pf; }
 int mt_opt_coschedule() { return g_coschedule; }
 int mt_opt_coschedule_pct() { return g_cosched_pct; }
 
@@ -289,6 +291,7 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 10) { old = g_coschedule; g_coschedule = value; }
   else if (option == 11) { old = g_cosched_pct; g_cosched_pct = value; }
   else if (option == 12) { old = g_wide_items; g_wide_items = value; }
+  else if (option == 13) { old = g_wide_l2pf; g_wide_l2pf = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

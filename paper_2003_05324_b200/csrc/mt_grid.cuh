@@ -280,6 +280,7 @@ int mt_opt_c_prefetch();
 int mt_opt_tc_diag();
 int mt_opt_cta_pairs();
 int mt_opt_wide_items();
+int mt_opt_wide_l2pf();
 bool mt_tc2w_supported(const Grid& g);
 int mt_tc2w_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st,
                    unsigned long long* span);

@@ -61,6 +61,7 @@ struct WorkW {
   int nsubm;
   int* counter;  // [work queue head, unused]
   unsigned long long* span;
+  int l2pf;      // stage each warp's C rows in L2 at item start (option 13)
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
@@ -250,6 +251,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         ++gl;
       };
       for (int c = 0; c < 3; ++c) load_chunk(c, (int)gu - (int)gl + 3);
+      if (w.l2pf && lane == 0) {
+        // the TMEM drain is on the MMA's critical path (single-buffered): stage the
+        // rest of this warp's C rows (32 x 2 KB) in L2 while the MMAs run
+        const float* crow_p = g.stile(i, j) + (int64_t)(m0 + q * 32) * nb;
+        for (int r = 0; r < 32; ++r)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(crow_p + (int64_t)r * nb),
+                       "r"(nb * 4)
+                       : "memory");
+      }
       mbar_wait(tfull, li & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -332,6 +342,7 @@ int mt_tc2w_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cud
   w.nsubm = g.nb / (2 * BM);
   w.nitems = (int)(scnt * w.nsubm);
   w.span = span;
+  w.l2pf = mt_opt_wide_l2pf();
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_smw) cudaDeviceGetAttribute(&g_smw, cudaDevAttrMultiProcessorCount, dev);
