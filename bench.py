@@ -322,12 +322,15 @@ def run_ours(args, rank, world, local_rank):
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
         key = f"n{n}_nb{nb}_t{t}"
-        # the bulk update launches (largest grid) of the CTA-pair kernel
-        cands = sorted((v["avg_duration_ms"], v["dram_bytes_per_launch"])
-                       for name, v in tr.get(key, {}).items()
-                       if name.startswith("tc2w_update_kernel") or name.startswith("tc2_update_kernel"))
-        if cands:
-            traffic = cands[-1][1]
+        # the bulk-update kernel's launches (tc2w: every launch is a bulk update)
+        ent = tr.get(key, {})
+        if "tc2w_update_kernel" in ent:
+            traffic = ent["tc2w_update_kernel"]["dram_bytes_per_launch"]
+        else:
+            cands = sorted((v["avg_duration_ms"], v["dram_bytes_per_launch"])
+                           for name, v in ent.items() if name.startswith("tc2_update_kernel"))
+            if cands:
+                traffic = cands[-1][1]
     except Exception:
         traffic = None
     fl_plan = mt.planned_flops(n, nb, mp_pol)
@@ -352,8 +355,9 @@ def run_ours(args, rank, world, local_rank):
                      "by the share of SMs the launch was given; algorithmic flops = reference "
                      "flop model (factor.py:83-95) per launch"),
         "share_of_step": d["ms"] / (t_dev / args.steps * 1e3),
-        "traffic_source": ("profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk launch "
-                           "(grid 296) of the bench command; above the algorithmic C read+write "
+        "traffic_source": ("profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk-update "
+                           "launch (tc2w_update_kernel, one evaluation at the bench config); above "
+                           "the algorithmic C read+write "
                            "because the A-panel rows are re-fetched per output column (the panel, "
                            "2 MB/tile, exceeds L2); the kernel is tensor-bound at ~54% of HBM "
                            "bandwidth (DESIGN.md section 4)"),

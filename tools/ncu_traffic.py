@@ -34,7 +34,9 @@ def summarise(path):
         per[lid][d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * SCALE.get(d["Metric Unit"], 1.0)
     # split a kernel's launches by grid size when recorded (bulk vs panel-column updates)
     for lid, ms in per.items():
-        if "launch__grid_size" in ms and names[lid].startswith(("tc2_update_kernel", "tc2w_update_kernel")):
+        # tc2_update_kernel serves both the bulk and the panel-column update: split by
+        # grid; the co-scheduled tc2w bulk kernel has a per-step grid, keep it whole
+        if "launch__grid_size" in ms and names[lid].startswith("tc2_update_kernel"):
             names[lid] += f"[grid={int(ms['launch__grid_size'])}]"
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for lid, ms in per.items():
