@@ -37,8 +37,11 @@ constexpr int HALF = A_BYTES + 2 * BH_BYTES;  // hi or lo part of a stage: 24 KB
 constexpr int STAGE_BYTES = 2 * HALF;         // 48 KB
 constexpr int NUM_THREADS = 192;
 constexpr int EPI_WARPS = 4;
-constexpr int CSLOTS = 4, CSLOT_BYTES = 32 * 32 * 4;
-constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 64 KB
+#ifndef MT_TC2W_CSLOTS
+#define MT_TC2W_CSLOTS 4
+#endif
+constexpr int CSLOTS = MT_TC2W_CSLOTS, CSLOT_BYTES = 32 * 32 * 4;  // loads CSLOTS-1 chunks ahead
+constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 64 KB at 4 slots
 constexpr int TMEM_COLS = 512;  // one 128 x 512 accumulator per CTA
 constexpr int SCHED = 4;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 640;
@@ -240,7 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const int crow = (int)((g.scol(j) + (i - j - g.t)) * (int64_t)nb) + m0 + q * 32;
       auto load_chunk = [&](int c, int newer) {
         if (lane == 0) {
-          if (newer >= 3) bulk_wait_read<3>();
+          if (newer >= 4) bulk_wait_read<4>();
+          else if (newer == 3) bulk_wait_read<3>();
           else if (newer == 2) bulk_wait_read<2>();
           else if (newer == 1) bulk_wait_read<1>();
           else bulk_wait_read<0>();
@@ -250,7 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         ++gl;
       };
-      for (int c = 0; c < 3; ++c) load_chunk(c, (int)gu - (int)gl + 3);
+      for (int c = 0; c < CSLOTS - 1; ++c) load_chunk(c, (int)gu - (int)gl + CSLOTS - 1);
       if (w.l2pf && lane == 0) {
         // the TMEM drain is on the MMA's critical path (single-buffered): stage the
         // rest of this warp's C rows (32 x 2 KB) in L2 while the MMAs run
@@ -303,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           bulk_commit();
         }
         ++gu;
-        if (c + 3 < NCH) load_chunk(c + 3, (int)gu - (int)gl + 3);
+        if (c + CSLOTS - 1 < NCH) load_chunk(c + CSLOTS - 1, (int)gu - (int)gl + CSLOTS - 1);
       }
     }
     if (lane == 0) bulk_wait_all();
