@@ -156,9 +156,7 @@ __global__ void __launch_bounds__(256) gen_kernel(Grid g, const double2* __restr
     T out[W];
     double2 pr = make_double2(0.0, 0.0);
     if (gr < n) pr = locs[gr];
-#pragma unroll
-    for (int q = 0; q < W; ++q) {
-      if (q >= w) break;
+    auto elem = [&](int q) -> T {
       const int64_t gc = (int64_t)j * nb + c0 + q;
       double v;
       if (gr >= n || gc >= n) {
@@ -169,10 +167,36 @@ __global__ void __launch_bounds__(256) gen_kernel(Grid g, const double2* __restr
       if constexpr (sizeof(T) == 4) {
         float f = __double2float_rn(v);
         if (isfinite(v) && !isfinite(f)) ++local_overflow;
-        out[q] = f;
+        return f;
       } else {
-        out[q] = v;
+        return v;
       }
+    };
+    if (vec && th.kind == 0 && gr < n && (int64_t)j * nb + c0 + W <= n) {
+      // nu = 1/2 interior: W independent inline FP64 chains (hypot, divide, exp;
+      // same operations and order as mt_matern_value) that the compiler can
+      // interleave -- generation is latency-bound on these chains
+      double v[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const double2 pc = locs[(int64_t)j * nb + c0 + q];
+        v[q] = th.variance * exp(-(dist(pr, pc, metric, radius) / th.spatial_range));
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        if constexpr (sizeof(T) == 4) {
+          const float f = __double2float_rn(v[q]);
+          if (isfinite(v[q]) && !isfinite(f)) ++local_overflow;
+          out[q] = f;
+        } else {
+          out[q] = v[q];
+        }
+      }
+    } else if (vec) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) out[q] = elem(q);
+    } else {
+      out[0] = elem(0);
     }
     T* dst = tile + (int64_t)r * nb + c0;
     if (vec) {
