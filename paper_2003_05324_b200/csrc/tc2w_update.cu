@@ -30,13 +30,21 @@ constexpr int BM = 128;     // accumulator rows per CTA (pair M = 256)
 constexpr int BNM = 256;    // N of one MMA
 constexpr int BNI = 512;    // N of a work item (two MMAs per product)
 constexpr int BNH = 128;    // rows of B each CTA stages per MMA half
-constexpr int BK = 16, STAGES = 3;
+#ifndef MT_TC2W_STAGES
+#define MT_TC2W_STAGES 3
+#endif
+#ifndef MT_TC2W_EPIW
+#define MT_TC2W_EPIW 4
+#endif
+constexpr int BK = 16, STAGES = MT_TC2W_STAGES;
 constexpr int A_BYTES = BM * BK * 4;    // 8 KB
 constexpr int BH_BYTES = BNH * BK * 4;  // 8 KB per half
 constexpr int HALF = A_BYTES + 2 * BH_BYTES;  // hi or lo part of a stage: 24 KB
 constexpr int STAGE_BYTES = 2 * HALF;         // 48 KB
-constexpr int NUM_THREADS = 192;
-constexpr int EPI_WARPS = 4;
+// epilogue warps: 4 (one per TMEM lane quadrant) or 8 (two per quadrant, each
+// draining half of the item's columns)
+constexpr int EPI_WARPS = MT_TC2W_EPIW;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 #ifndef MT_TC2W_CSLOTS
 #define MT_TC2W_CSLOTS 4
 #endif
@@ -234,7 +242,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint64_t* wbar = cbar + (warp - 2) * CSLOTS;
     uint32_t gl = 0, gu = 0;
     const uint32_t tempty_leader = peer_addr(tempty, 0);
-    constexpr int NCH = BNI / 32;  // 16 chunks of 32 columns per warp and item
+    constexpr int NCH = BNI / 32 / (EPI_WARPS / 4);  // chunks of 32 columns per warp and item
+    const int cbase = ((warp - 2) / 4) * NCH;        // this warp's first chunk
     for (uint32_t li = 0;; ++li) {
       int i, j;
       const int item = next_item(li, &i, &j);
@@ -250,12 +259,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           else bulk_wait_read<0>();
           const uint32_t s = gl % CSLOTS;
           mbar_expect_tx(&wbar[s], CSLOT_BYTES);
-          tma_load_2d(wslots + s * CSLOT_BYTES, &map_c, &wbar[s], c * 32, crow);
+          tma_load_2d(wslots + s * CSLOT_BYTES, &map_c, &wbar[s], (cbase + c) * 32, crow);
         }
         ++gl;
       };
       for (int c = 0; c < CSLOTS - 1; ++c) load_chunk(c, (int)gu - (int)gl + CSLOTS - 1);
-      if (w.l2pf && lane == 0) {
+      if (w.l2pf && lane == 0 && cbase == 0) {
         // the TMEM drain is on the MMA's critical path (single-buffered): stage the
         // rest of this warp's C rows (32 x 2 KB) in L2 while the MMAs run
         const float* crow_p = g.stile(i, j) + (int64_t)(m0 + q * 32) * nb;
@@ -279,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
               "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
               "=r"(v[31])
-            : "r"(taddr + c * 32));
+            : "r"(taddr + (cbase + c) * 32));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == NCH - 1) {
           // the whole accumulator is in registers now: let the next item's MMAs start
@@ -303,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&map_c, wslots + s * CSLOT_BYTES, c * 32, crow);
+          tma_store_2d(&map_c, wslots + s * CSLOT_BYTES, (cbase + c) * 32, crow);
           bulk_commit();
         }
         ++gu;
