@@ -177,6 +177,26 @@ def krige_case():
     print("krige", meta)
 
 
+def strong_npd_case():
+    """configs[2]-shaped field at N=16384: the reference's MP (t=8) is indefinite;
+    record its FactorizationError index (the GPU RN engine must match it)."""
+    n = 16384
+    locs = geodata.generate_locations(n, seed=geodata.derive_seed(3, 0))
+    ds, _ = geodata.morton_sort(geodata.GeoDataset(locs, np.random.default_rng(3).standard_normal(n)))
+    try:
+        mle.loglik(ds, covmath.MaternParams(1.0, 0.3, 1.0), 512, PP.mp(diag_thick=8))
+        idx = None
+    except factor.FactorizationError as exc:
+        idx = exc.index
+    json.dump({"recipe": "generate_locations(16384, seed=derive_seed(3,0)); z = default_rng(3)."
+                         "standard_normal(n); morton_sort; loglik(theta=(1.0, 0.3, 1.0), nb=512, "
+                         "PrecisionPolicy.mp(diag_thick=8))",
+               "n": n, "nb": 512, "theta": [1.0, 0.3, 1.0], "band_t": 8,
+               "reference_factorization_error_index": idx},
+              open(os.path.join(OUT, "strong16384_npd.json"), "w"), indent=1)
+    print("strong16384 npd", idx)
+
+
 def main():
     print("reference mixtile", mixtile.__version__)
     th1 = covmath.MaternParams(1.0, 0.1, 0.5)
@@ -197,6 +217,7 @@ def main():
     flops_case()
     fit_case()
     krige_case()
+    strong_npd_case()
 
 
 if __name__ == "__main__":

@@ -167,3 +167,29 @@ def test_evaluator_split_launch_equals_fused(gpu):
     split = ev.finish()
     assert split == fused
     assert e[0].elapsed_time(e[1]) > 0.0
+
+
+def test_strong_field_mp_indefinite_like_reference(gpu):
+    """configs[2]-shaped field (beta=0.3, nu=1) at N=16384: the reference's MP
+    (t=8) factorization is indefinite (tests/golden/strong16384_npd.json).  The
+    GPU MP path must raise FactorizationError too; the round-to-nearest FFMA
+    engine fails at the reference's exact global pivot."""
+    import json
+    import os
+    from conftest import GOLDEN
+    mt = _mt()
+    g = json.load(open(os.path.join(GOLDEN, "strong16384_npd.json")))
+    n = g["n"]
+    locs = mt.generate_locations(n, seed=mt.derive_seed(3, 0))
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.random.default_rng(3).standard_normal(n)))
+    pol = mt.PrecisionPolicy.mp(diag_thick=g["band_t"])
+    th = mt.MaternParams(*g["theta"])
+    old = mt.set_fp32_engine("ffma")
+    try:
+        with pytest.raises(mt.FactorizationError) as exc:
+            mt.loglik(ds, th, g["nb"], pol)
+        assert exc.value.index == g["reference_factorization_error_index"]
+    finally:
+        mt.set_fp32_engine(old)
+    with pytest.raises(mt.FactorizationError):
+        mt.loglik(ds, th, g["nb"], pol)
