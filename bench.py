@@ -62,8 +62,11 @@ def parse():
     ap.add_argument("--t", type=int, default=8)
     ap.add_argument("--dp-n", type=int, default=65536,
                     help="N of the MP-vs-DP comparison when full DP at --n does not fit")
-    ap.add_argument("--dp-t", type=int, default=2)
+    ap.add_argument("--dp-t", type=int, default=8,
+                    help="MP band of the MP-vs-DP comparison at --dp-n (default: the headline t)")
     ap.add_argument("--cpu-n", type=int, default=16384, help="CPU baseline sample size")
+    ap.add_argument("--engine", default="tf32x3", choices=["tf32x3", "tf32x3_rz", "ffma"],
+                    help="off-band FP32 engine (default: the FP32-accurate tcgen05 engine)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dp", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -126,9 +129,37 @@ def load_peaks():
 
 
 # --------------------------------------------------------------- CPU baseline
+class _TimedKernels:
+    """Stand-in for the oracle's scipy BLAS/LAPACK modules that times every
+    call, split into FP64 kernels (dpotrf/dtrsm/dsyrk/dgemm) and FP32 kernels
+    (strsm/sgemm), so the Cholesky can be extrapolated by component."""
+
+    DP = ("dpotrf", "dtrsm", "dsyrk", "dgemm")
+    SP = ("strsm", "sgemm")
+
+    def __init__(self, mod, acc):
+        self._m, self._acc = mod, acc
+
+    def __getattr__(self, name):
+        fn = getattr(self._m, name)
+        kind = "dp" if name in self.DP else ("sp" if name in self.SP else None)
+        if kind is None:
+            return fn
+
+        def timed(*a, **kw):
+            t0 = time.perf_counter()
+            try:
+                return fn(*a, **kw)
+            finally:
+                self._acc[kind] += time.perf_counter() - t0
+        return timed
+
+
 def cpu_reference_sample(n, nb, t, reps=1):
     """Time the reference algorithm (oracle port) for one MP evaluation at n on
-    all host cores; returns (seconds per eval, cholesky seconds, cores, info)."""
+    all host cores, by component: assembly, the Cholesky's FP64 and FP32
+    kernels, the rest of the Cholesky (task loop, conversions), logdet + solve.
+    Returns (seconds per eval, components dict, cores, info)."""
     import numpy as np
     from threadpoolctl import threadpool_info, threadpool_limits
 
@@ -139,19 +170,29 @@ def cpu_reference_sample(n, nb, t, reps=1):
     locs = generate_locations(n, seed=derive_seed(0, 0))
     ds, _ = morton_sort(GeoDataset(locs, np.random.default_rng(7).standard_normal(n)))
     t = min(t, -(-n // nb))
-    best = best_chol = float("inf")
+    best, comp = float("inf"), None
+    saved = (O._blas, O._lapack)
     with threadpool_limits(limits=cores):
         for _ in range(reps):
-            t0 = time.perf_counter()
-            tiles = O.assemble(ds.locations, THETA, nb, "mp", t)
-            t1 = time.perf_counter()
-            fac = O.cholesky(tiles, n, nb, "mp", t)
-            t2 = time.perf_counter()
-            O.logdet(fac, -(-n // nb))
-            float(ds.z @ O.solve(fac, n, nb, ds.z))
-            t3 = time.perf_counter()
-            best = min(best, t3 - t0)
-            best_chol = min(best_chol, t2 - t1)
+            acc = {"dp": 0.0, "sp": 0.0}
+            O._blas, O._lapack = _TimedKernels(saved[0], acc), _TimedKernels(saved[1], acc)
+            try:
+                t0 = time.perf_counter()
+                tiles = O.assemble(ds.locations, THETA, nb, "mp", t)
+                t1 = time.perf_counter()
+                fac = O.cholesky(tiles, n, nb, "mp", t)
+                t2 = time.perf_counter()
+                O.logdet(fac, -(-n // nb))
+                float(ds.z @ O.solve(fac, n, nb, ds.z))
+                t3 = time.perf_counter()
+            finally:
+                O._blas, O._lapack = saved
+            if t3 - t0 < best:
+                best = t3 - t0
+                comp = {"assemble_s": t1 - t0, "cholesky_s": t2 - t1, "chol_fp64_kernels_s": acc["dp"],
+                        "chol_fp32_kernels_s": acc["sp"],
+                        "chol_other_s": max(0.0, (t2 - t1) - acc["dp"] - acc["sp"]),
+                        "logdet_solve_s": t3 - t2}
         libs = [f"{d.get('internal_api')}:{d.get('num_threads')}" for d in threadpool_info()]
     cpu = ""
     try:
@@ -159,23 +200,57 @@ def cpu_reference_sample(n, nb, t, reps=1):
             cpu = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "")
     except OSError:
         pass
-    return best, best_chol, cores, {"cpu_model": cpu, "blas_threads": libs}
+    return best, comp, cores, {"cpu_model": cpu, "blas_threads": libs}
+
+
+def extrapolate_cpu(comp, n_s, n, nb, t):
+    """Seconds per evaluation at n from a sample at n_s, by component:
+    assembly and logdet+solve scale with the matrix size (N^2); the Cholesky's
+    FP64 and FP32 kernels run at their measured rates over the planned FP64 /
+    FP32 flops at n (factor.py:134-145, so the band's share is right at both
+    sizes); the task loop scales with the task count (p^3)."""
+    from oracle import mixtile_oracle as O
+    ps, p = -(-n_s // nb), -(-n // nb)
+    fdp_s, fsp_s = O.planned_flops(n_s, nb, "mp", min(t, ps))
+    fdp, fsp = O.planned_flops(n, nb, "mp", min(t, p)) if p <= 64 else _planned_closed(n, nb, t)
+    r_dp = fdp_s / max(comp["chol_fp64_kernels_s"], 1e-9)
+    r_sp = fsp_s / max(comp["chol_fp32_kernels_s"], 1e-9)
+    parts = {
+        "assemble_s": comp["assemble_s"] * (n / n_s) ** 2,
+        "chol_fp64_kernels_s": fdp / r_dp,
+        "chol_fp32_kernels_s": fsp / r_sp,
+        "chol_other_s": comp["chol_other_s"] * (p / ps) ** 3,
+        "logdet_solve_s": comp["logdet_solve_s"] * (n / n_s) ** 2,
+    }
+    return sum(parts.values()), parts, {"cpu_fp64_gflops": r_dp / 1e9, "cpu_fp32_gflops": r_sp / 1e9}
+
+
+def _planned_closed(n, nb, t):
+    """(F_dp, F_sp) of an MP plan with uniform tiles (SURVEY.md 8d closed form)."""
+    p = n // nb
+    s1 = sum(p - d for d in range(1, t))
+    s2 = sum((p - 1 - d) * (p - d) / 2 for d in range(1, t))
+    fdp = nb ** 3 * (p / 3 + p * (p - 1) / 2 + s1 + 2 * s2)
+    return fdp, n ** 3 / 3 - fdp
 
 
 def cpu_baseline_obj(args):
-    sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t, reps=2)
-    scale = (args.cpu_n / args.n) ** 3
+    sec, comp, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t, reps=2)
+    ext, parts, rates = extrapolate_cpu(comp, args.cpu_n, args.n, args.nb, args.t)
     return {
-        "value": (1.0 / sec) * scale,
+        "value": 1.0 / ext,
         "unit": UNIT,
         "cores": cores,
         "kind": "port",
         "sample": (f"oracle port of the reference (same dpotrf/dtrsm/strsm/dsyrk/dgemm/sgemm "
-                   f"calls), best of 2 MP t={min(args.t, args.cpu_n // args.nb)} nb={args.nb} "
-                   f"evaluations at N={args.cpu_n}: {sec:.2f} s ({chol:.2f} s Cholesky = "
-                   f"{args.cpu_n ** 3 / 3 / chol / 1e9:.1f} GFLOP/s); value extrapolated to "
-                   f"N={args.n} by the N^3 flop count"),
-        "cpu_cholesky_gflops": args.cpu_n ** 3 / 3 / chol / 1e9,
+                   f"calls; bitwise-pinned to reference goldens), best of 2 MP t="
+                   f"{min(args.t, args.cpu_n // args.nb)} nb={args.nb} evaluations at N={args.cpu_n}: "
+                   f"{sec:.2f} s; extrapolated to N={args.n} by component (assembly and solve "
+                   f"by N^2, FP64/FP32 kernels by their planned flops at their measured rates, "
+                   f"task loop by p^3): {ext:.0f} s per evaluation"),
+        "sample_components_s": comp,
+        "extrapolated_components_s": parts,
+        **rates,
         **info,
     }
 
@@ -185,27 +260,49 @@ def run_reference(args, rank):
         return
     for _ in range(max(0, args.warmup)):
         cpu_reference_sample(args.cpu_n, args.nb, args.t)
-    times = []
-    cores, info = 1, {}
+    exts = []
+    cores, info, parts, rates = 1, {}, {}, {}
     for _ in range(max(1, args.steps)):
-        sec, chol, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t)
-        times.append(sec)
-    sec = sum(times) / len(times)
-    value = (1.0 / sec) * (args.cpu_n / args.n) ** 3
+        sec, comp, cores, info = cpu_reference_sample(args.cpu_n, args.nb, args.t)
+        ext, parts, rates = extrapolate_cpu(comp, args.cpu_n, args.n, args.nb, args.t)
+        exts.append(ext)
+    sec = sum(exts) / len(exts)
+    value = 1.0 / sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-        "config": {"workload": f"MP t={args.t} nb={args.nb} loglik at N={args.n}: sampled at "
-                               f"N={args.cpu_n} on the host CPU, extrapolated by N^3",
+        "config": {"workload": f"MP t={args.t} nb={args.nb} loglik at N={args.n}: each step one "
+                               f"evaluation sampled at N={args.cpu_n} on the host CPU, "
+                               f"extrapolated by component",
                    "n": args.n, "nb": args.nb, "band_t": args.t},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"one MP evaluation at N={args.cpu_n} per step "
-                                   f"(oracle port, all host threads), extrapolated by N^3", **info},
+                         "sample": f"one MP evaluation at N={args.cpu_n} per step (oracle port of "
+                                   f"the reference, all host threads), extrapolated to N={args.n} "
+                                   f"by component (assembly/solve N^2, FP64/FP32 kernels by planned "
+                                   f"flops at measured rates, task loop p^3)",
+                         "extrapolated_components_s": parts, **rates, **info},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def fp64_peaks(lib, seconds=4.0):
+    """FP64 DMMA peak of this GPU: (burst, sustained) TFLOP/s.  Burst = best of
+    5 short probe launches; sustained = median launch while probing back to
+    back for `seconds` (the way MEASURED_PEAKS.json measures bf16)."""
+    v = ctypes.c_double()
+    burst = 0.0
+    for _ in range(5):
+        lib.mt_peak_probe(2, 20000, ctypes.byref(v))
+        burst = max(burst, v.value)
+    rates, t0 = [], time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        lib.mt_peak_probe(2, 20000, ctypes.byref(v))
+        rates.append(v.value)
+    rates.sort()
+    return burst, rates[len(rates) // 2]
 
 
 # ------------------------------------------------------------------- GPU arm
@@ -259,6 +356,8 @@ def run_ours(args, rank, world, local_rank):
         return ev.finish()
 
     n, nb, t = args.n, args.nb, args.t
+    engine = args.engine
+    mt.set_fp32_engine(engine)
     ds = _dataset(mt, n)  # same dataset on every rank (one distributed evaluation)
     theta = mt.MaternParams(*THETA)
     mp_pol = mt.PrecisionPolicy.mp(diag_thick=t)
@@ -314,46 +413,48 @@ def run_ours(args, rank, world, local_rank):
     achieved = d["flops"] / (d["ms_sm_weighted"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
     achieved_raw = d["flops"] / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else 0.0
     p32 = bf16_sus / 6.0  # tcgen05 kind::tf32 = bf16 rate / 2; 3xTF32 = 3 MMAs per FP32 product
-    p64c = ctypes.c_double()
-    lib.mt_peak_probe(2, 20000, ctypes.byref(p64c))
-    p64 = max_over_ranks(p64c.value) if dist_on else p64c.value
+    p64_burst, p64_sus = fp64_peaks(lib)
+    p64_burst, p64_sus = max_over_ranks(p64_burst), max_over_ranks(p64_sus)
+    p64 = p64_sus  # the factorization is a long step: sustained, like P32
     traffic = None
+    dom_kernel = {"tf32x3": "tcf_update_kernel", "tf32x3_rz": "tc2w_update_kernel"}.get(
+        engine, "sgemm_update_kernel")
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
-        key = f"n{n}_nb{nb}_t{t}"
-        # the bulk-update kernel's launches (tc2w: every launch is a bulk update)
-        ent = tr.get(key, {})
-        if "tc2w_update_kernel" in ent:
-            traffic = ent["tc2w_update_kernel"]["dram_bytes_per_launch"]
-        else:
-            cands = sorted((v["avg_duration_ms"], v["dram_bytes_per_launch"])
-                           for name, v in ent.items() if name.startswith("tc2_update_kernel"))
-            if cands:
-                traffic = cands[-1][1]
+        ent = tr.get(f"n{n}_nb{nb}_t{t}", {})
+        cands = sorted((v["avg_duration_ms"], v["dram_bytes_per_launch"])
+                       for name, v in ent.items() if name.startswith(dom_kernel))
+        if cands:  # the longest launches are the bulk updates
+            traffic = cands[-1][1]
     except Exception:
         traffic = None
     fl_plan = mt.planned_flops(n, nb, mp_pol)
     t_roof = (fl_plan.sp / (p32 * 1e12) + fl_plan.dp / (p64 * 1e12)) / world
     roofline = {
-        "bound": "tensor", "achieved": achieved, "peak": p32, "unit": "TFLOP/s",
-        "frac": achieved / p32, "traffic": traffic,
-        "kernel": "tc2w_update_kernel (CTA pairs, tcgen05.mma.cta_group::2, 256x512 items)",
-        "pipe": "tcgen05.mma kind::tf32 (3xTF32 FP32 emulation), TMEM accumulators, TMA",
+        "bound": "tensor", "achieved": achieved_raw, "peak": p32, "unit": "TFLOP/s",
+        "frac": achieved_raw / p32, "traffic": traffic,
+        "kernel": f"{dom_kernel} (CTA pairs, tcgen05.mma.cta_group::2)",
+        "pipe": ("tcgen05.mma kind::tf32 (3xTF32 FP32 emulation), TMEM chunk accumulators "
+                 "flushed into round-to-nearest FP32 sums every 32 K-columns, TMA"
+                 if engine == "tf32x3" else engine),
         "peak_source": (f"{peak_src}: bf16_tflops_sustained {bf16_sus:.0f} / 2 (TF32 rate) / 3 "
                         "(MMAs per FP32 product); sustained figure since the kernel runs inside "
                         "a long step"),
         "launches_per_step": d["launches"],
         "avg_launch_ms": d["ms"] / max(1, d["launches"]),
         "avg_sm_share": sm_share,
-        "achieved_on_its_sms_only_raw": achieved_raw,
+        "achieved_per_sm_share": achieved,
+        "frac_per_sm_share": achieved / p32,
+        "frac_note": ("frac = achieved / peak with achieved = flops / device span of the launches "
+                      "(raw); *_per_sm_share divides by span x the SM share the co-scheduled "
+                      "launch was given (its rate per whole-GPU equivalent)"),
         "algorithmic_flops_per_launch": d["flops"] / max(1, d["launches"]),
         "algorithmic_bytes_per_launch": d["bytes"] / max(1, d["launches"]),
         "measured": ("device-side %globaltimer span of every bulk trailing-update launch inside "
                      "the timed region (it runs concurrently with the co-scheduled FP64 band "
-                     "update on the same stream, so stream events cannot bracket it), weighted "
-                     "by the share of SMs the launch was given; algorithmic flops = reference "
-                     "flop model (factor.py:83-95) per launch"),
+                     "update on the same stream, so stream events cannot bracket it); "
+                     "algorithmic flops = reference flop model (factor.py:83-95) per launch"),
         "share_of_step": d["ms"] / (t_dev / args.steps * 1e3),
         "traffic_source": ("profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk-update "
                            "launch (tc2w_update_kernel, one evaluation at the bench config); above "
@@ -365,8 +466,12 @@ def run_ours(args, rank, world, local_rank):
             "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
             "f_sp": fl_plan.sp, "f_dp": fl_plan.dp,
             "p32_tflops": p32, "p64_tflops": p64,
-            "p32_source": "bf16_sustained/6 (3xTF32 on tcgen05)",
-            "p64_source": "mt_peak_probe: FP64 DMMA m8n8k4 chains on all SMs, this run"},
+            "p32_source": "MEASURED_PEAKS.json bf16_sustained/6 (3xTF32 on tcgen05)",
+            "p64_burst_tflops": p64_burst, "p64_sustained_tflops": p64_sus,
+            "p64_source": ("mt_peak_probe (csrc/prof.cu): independent FP64 DMMA m8n8k4 chains on "
+                           "every SM, this run; burst = best single ~10 ms launch, sustained = "
+                           "median launch over 4 s back to back (MEASURED_PEAKS.json has no "
+                           "FP64 figure)")},
     }
 
     # ---- e2e through the public API from host buffers (pools of the timed
@@ -474,9 +579,75 @@ def run_ours(args, rank, world, local_rank):
             "kernel_event_spans_ms_per_step": {k: round(v["ms"], 3) for k, v in kinds.items()},
             "mp_vs_dp": dp, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "clocks": clocks.summary(),
+            "nccl": ({"version": ".".join(map(str, torch.cuda.nccl.version())),
+                      "world_size": world, "backend": dist.get_backend(),
+                      "init_lines": nccl_summary()} if dist_on else None),
             "loglik_sample": results[-1],
         }
         print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks
+    (one process per GPU) with torch.distributed.run on 127.0.0.1 and return
+    its exit code.  Rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ))
+
+
+def nccl_debug_env():
+    """NCCL's communicator-init lines (rank count, transports, NVLS) go to a
+    per-process file, not to stdout (which carries the JSON line)."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(
+        os.environ.get("MT_NCCL_LOG_DIR", "/tmp"), "mt_bench_nccl.%h.%p.log"))
+
+
+def nccl_summary():
+    """Init lines of this run's NCCL logs (rank 0 reports them)."""
+    import glob
+    pat = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", "*").replace("%p", "*")
+    lines = []
+    for f in sorted(glob.glob(pat)) if pat else []:
+        try:
+            if os.path.getmtime(f) < _T_START:
+                continue
+            with open(f) as fh:
+                lines += [ln.strip() for ln in fh if "Init COMPLETE" in ln or "nranks" in ln]
+        except OSError:
+            pass
+    return lines[:16]
+
+
+_T_START = time.time()
+
+
+def run_dry(args, rank, world):
+    """Launch/rendezvous check without a GPU (MT_BENCH_DRYRUN=1, gloo): every
+    rank joins, the max-over-ranks reduction runs, rank 0 prints the line
+    shape with n_gpus = world size.  Never used for reported numbers."""
+    import torch
+    import torch.distributed as dist
+    seen = torch.tensor([1.0])
+    t = torch.tensor([float(rank + 1)])
+    if world > 1:
+        dist.all_reduce(seen)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                          "dry_run": True, "ranks_joined": int(seen.item()),
+                          "max_over_ranks": t.item(), "steps": args.steps,
+                          "warmup": args.warmup}), flush=True)
 
 
 def main():
@@ -484,25 +655,37 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":  # the CPU arm is rank 0's alone; no ranks to spawn
+            run_reference(args, 0)
+            return
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    dry = os.environ.get("MT_BENCH_DRYRUN") == "1"
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank % torch.cuda.device_count())
-        # high-priority NCCL streams: the panel broadcasts get SMs ahead of the
-        # bulk update's pending CTAs (which also yield on request)
-        if os.environ.get("MT_BENCH_BACKEND", "nccl") == "gloo":
-            # dev check of the multi-rank bench logic on a one-GPU box (ranks share cuda:0;
-            # NCCL refuses that); never used for reported numbers
+        if dry or os.environ.get("MT_BENCH_BACKEND", "nccl") == "gloo":
+            # dev checks of the multi-rank logic: CPU-only (dry run) or ranks
+            # sharing one GPU (NCCL refuses that); never used for reported numbers
+            if not dry:
+                torch.cuda.set_device(local_rank % torch.cuda.device_count())
             dist.init_process_group("gloo")
         else:
+            nccl_debug_env()
+            torch.cuda.set_device(local_rank % torch.cuda.device_count())
+            # high-priority NCCL streams: the panel broadcasts get SMs ahead of the
+            # bulk update's pending CTAs (which also yield on request)
             opts = dist.ProcessGroupNCCL.Options()
             opts.is_high_priority_stream = True
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
                                     pg_options=opts)
-    run_ours(args, rank, world, local_rank)
+    if dry:
+        run_dry(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -248,7 +248,9 @@ int mt_prof_sm_weighted(int32_t nkinds, double* ms_w);
 int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
 
 /* Runtime options; returns the previous value.
- *   0: FP32 (off-band) update engine: 0 = SIMT FFMA, 1 = tcgen05 3xTF32 (default)
+ *   0: FP32 (off-band) update engine: 0 = SIMT FFMA, 1 = tcgen05 3xTF32 with
+ *      round-to-nearest chunk accumulation (default), 2 = tcgen05 3xTF32 with
+ *      whole-K TMEM accumulation (round-toward-zero; faster, opt-in)
  *   1: CTA cap of the bulk trailing update (0 = all SMs)
  *   2: 1 = register-staged DMMA band update instead of the TMA-staged one
  *   3: off-band panel TRSM: 1 = tcgen05 3xTF32 GEMM against L_kk^{-1} (default),

@@ -24,7 +24,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE
           "--expt-relaxed-constexpr"]
 # per-unit extra flags: generation rounds like numpy (no FMA contraction)
 EXTRA = {"gen.cu": ["-fmad=false"]}
-UNITS = ["api.cu", "gen.cu", "potrf.cu", "trsm.cu", "update.cu", "solve.cu", "prof.cu", "tc_update.cu", "tc2_update.cu", "tc2w_update.cu", "dmma_update.cu"]
+UNITS = ["api.cu", "gen.cu", "potrf.cu", "trsm.cu", "update.cu", "solve.cu", "prof.cu", "tc_update.cu", "tc2_update.cu", "tc2w_update.cu", "tcf_update.cu", "dmma_update.cu"]
 
 
 def _nvcc():

@@ -187,8 +187,10 @@ static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main,
     if (k + 2 < p) {
       const std::function<int()> ask = [&]() { return request((unsigned)ysms); };
       RC(mt_trsm_impl(g, k + 1, pan, yield_on ? &ask : nullptr));
-      RC(request(0u));
     }
+    // withdraw the request after every panel (also the last one, so the word
+    // never carries into the next factorization or a later bulk update)
+    RC(request(0u));
     RC(fwd_step(k + 1, pan));  // panel k+1 is final
     // caller stream: the rest of step k's trailing update
     RC(mt_update_impl(gb, k, k + 2, p, main));
@@ -262,7 +264,8 @@ extern "C" {
 
 int32_t mt_version(void) { return 11; }
 
-/* option 0: FP32 update engine (0 FFMA SIMT, 1 tcgen05 3xTF32);
+/* option 0: FP32 update engine (0 FFMA SIMT, 1 tcgen05 3xTF32 round-to-nearest chunks,
+ *           2 tcgen05 3xTF32 whole-K TMEM accumulation);
  * option 1: CTA cap of the bulk trailing update (0 = all SMs);
  * option 2: 1 = legacy register-staged DMMA band update;
  * option 3: 1 = off-band TRSM as a tcgen05 GEMM against L_kk^{-1} (default),
@@ -626,6 +629,10 @@ int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t_, const doub
       al((void**)&d_work, mt_work_doubles(&t) * 8) || al((void**)&d_out, 16)) {
     rc = MT_E_CUDA;
   }
+  // the tensor-core engine's split buffer, as TileMatrix allocates it
+  // (tilestore.py): the C entry point runs the same kernels as the Python path
+  const int64_t nsplit = (mode == MT_MODE_MP && nb % 256 == 0) ? mt_split_tiles(t.p, t.t, mode) : 0;
+  if (!rc && nsplit > 0 && al((void**)&t.split, (size_t)nsplit * te * 4)) rc = MT_E_CUDA;
   if (!rc) {
     const int64_t init[4] = {-1, 0, 0, 0};
     cudaMemcpyAsync(t.status, init, sizeof(init), cudaMemcpyHostToDevice, st);
@@ -645,6 +652,7 @@ int mt_evaluate_host(int64_t n, int32_t nb, int32_t mode, int32_t t_, const doub
   }
   cudaFreeAsync(t.dp_pool, st); cudaFreeAsync(t.sp_pool, st); cudaFreeAsync(t.scratch, st);
   cudaFreeAsync(t.status, st); cudaFreeAsync(d_locs, st); cudaFreeAsync(d_z, st);
+  if (t.split) cudaFreeAsync(t.split, st);
   cudaFreeAsync(d_work, st); cudaFreeAsync(d_out, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);

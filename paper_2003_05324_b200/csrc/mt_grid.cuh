@@ -258,7 +258,11 @@ struct ProfScope {
 };
 
 // runtime options (api.cu): FP32 update engine and grid cap of the bulk update
-enum MtEngine { MT_ENGINE_FFMA = 0, MT_ENGINE_TF32X3 = 1 };
+// FP32 engines: SIMT FFMA; tcgen05 3xTF32 with round-to-nearest chunk
+// accumulation (default, FP32-accurate: tcf_update.cu); tcgen05 3xTF32 with the
+// whole K range in TMEM (round-toward-zero accumulation, faster, opt-in)
+enum MtEngine { MT_ENGINE_FFMA = 0, MT_ENGINE_TF32X3 = 1, MT_ENGINE_TF32X3_RZ = 2 };
+inline bool mt_engine_tc(int e) { return e == MT_ENGINE_TF32X3 || e == MT_ENGINE_TF32X3_RZ; }
 int mt_opt_engine();
 int mt_opt_update_ctas();
 int mt_opt_legacy_dmma();
@@ -284,6 +288,8 @@ int mt_opt_wide_l2pf();
 bool mt_tc2w_supported(const Grid& g);
 int mt_tc2w_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st,
                    unsigned long long* span);
+int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm, int presplit,
+                  cudaStream_t st, unsigned long long* span);
 int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
                   int presplit, cudaStream_t st, unsigned long long* span = nullptr, int jlo = 0,
                   int jhi = 0);

@@ -425,7 +425,7 @@ bool mt_tc_supported(const Grid& g) {
 }
 
 bool mt_tc_trsm_enabled(const Grid& g) {
-  return mt_opt_tc_trsm() && (mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) &&
+  return mt_opt_tc_trsm() && (mt_engine_tc(mt_opt_engine()) || g.cs > 1) &&
          mt_tc_supported(g);
 }
 
@@ -434,6 +434,11 @@ namespace {
 int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
                 cudaStream_t st, int jlo = 0, int jhi = 0, unsigned long long* span = nullptr) {
   if (scnt <= 0) return MT_OK;
+  // default engine: round-to-nearest chunked accumulation (tcf_update.cu); the
+  // kernels below accumulate the whole K range in TMEM (opt-in engine 2)
+  if (mt_opt_engine() != MT_ENGINE_TF32X3_RZ)
+    return mt_tcf_launch(g, k, s0, scnt, ctas, trsm, (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st,
+                         span);
   // full-width (256 x 512) CTA-pair items for the bulk update (tc2w_update.cu)
   if (!trsm && mt_opt_wide_items() && mt_opt_cta_pairs() && mt_tc2w_supported(g) && jlo > k + 1 &&
       !mt_opt_tc_diag() && !mt_opt_c_prefetch() && mt_opt_super_cols() == 0)

@@ -1,0 +1,517 @@
+// FP32-accurate 3xTF32 on CTA pairs: the off-band trailing update, the
+// panel-column update and the off-band panel TRSM with the TMEM accumulator
+// FLUSHED into a round-to-nearest FP32 running sum in registers every KC
+// K-slabs.
+//
+//   C_ij <- C_ij - A_ik A_jk^T      (kernels.gemm FP32 path, factor.py:273-274)
+//   X_ik  = B_ik W^T, W = L_kk^-1   (kernels.trsm FP32 path, factor.py:264)
+//
+// Why: tcgen05.mma adds every K=8 partial product into the FP32 TMEM
+// accumulator with round-toward-zero.  Over a 512-deep update that is 192
+// biased roundings at the magnitude of the running sum -- a systematic error
+// FP32 FFMA / OpenBLAS sgemm (round-to-nearest) does not have
+// (tools/emulate_tf32x3.py, tools/emulate_flush.py).  The bias of a chunk
+// grows with its length, so each accumulation restarts from zero every KC
+// slabs (KC = 2: 4 MMA k-steps, K = 32) and the epilogue adds the chunk into
+// its registers with ordinary round-to-nearest FADDs; C_new = RN(C - sum).
+// CPU emulation of exactly this arithmetic puts kriging within 1.3x of the
+// reference's sgemm deviation from DP (RZ unflushed: 12.6x).
+//
+// Layout (one CTA per SM, cluster (2,1,1), 320 threads):
+//   warp 0  TMA producer (+ the leader's dynamic work queue, as tc2_update.cu)
+//   warp 1  leader: tcgen05.mma.cta_group::2 issuer, M = 256, N = 256; the two
+//           TMEM buffers (256 columns each) alternate per K chunk, not per item
+//   warps 2..9  epilogue: two warps per TMEM lane quadrant, 128 columns each;
+//           128 running-sum registers per thread (lane = accumulator row).
+//           Per chunk: 4 tcgen05.ld 32x32b.x32 + FADDs (TMEM reads measured at
+//           ~26 B/clk per warp on B200, tools/tmem_bw.cu: 8 warps drain a
+//           128 KB chunk in ~0.6 us of the chunk's ~0.8 us of MMA).
+//           Item end: C streamed through 3 SWIZZLE_128B 32x32 chunk slots per
+//           warp with TMA (loaded during the item), result stored by TMA; the
+//           panel-column update and the TRSM also store the TF32 hi/lo split
+//           of their outputs (operands of the next step) by TMA.
+// Deterministic: every output element gets the same MMA and FADD sequence in
+// the same order from exactly one pair, whatever the schedule.
+#include <cuda.h>
+
+#include "tma.cuh"
+#include "tc2_common.cuh"
+
+namespace {
+using namespace mt_tma;
+using namespace mt_pair;
+
+constexpr int BM = 128;   // accumulator rows per CTA (pair M = 256)
+constexpr int BN = 256;   // pair N (one MMA)
+constexpr int BNH = 128;  // rows of B each CTA stages
+constexpr int BK = 16;
+#ifndef MT_TCF_KC
+#define MT_TCF_KC 2
+#endif
+constexpr int KC = MT_TCF_KC;  // K slabs per TMEM chunk
+static_assert(16 % KC == 0, "KC must divide the 16-slab item granularity");
+#ifndef MT_TCF_STAGES
+#define MT_TCF_STAGES 4
+#endif
+constexpr int STAGES = MT_TCF_STAGES;
+constexpr int A_BYTES = BM * BK * 4;                  // 8 KB
+constexpr int B_BYTES = BNH * BK * 4;                 // 8 KB
+constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
+constexpr int EPI_WARPS = 8;
+constexpr int COLS_W = BN / 2;  // columns per epilogue warp
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int CSLOTS = 3, CSLOT_BYTES = 32 * 32 * 4;
+constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 96 KB
+constexpr int TMEM_COLS = 512;                               // 2 chunk buffers x 256 columns
+constexpr int SCHED = 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 768;
+static_assert(SMEM_BYTES <= 232448, "shared memory");
+
+// kind::tf32, D f32, A/B tf32 K-major, N = 256, M = 256 (cta_group::2)
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void ld32(uint32_t (&v)[32], uint32_t taddr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void ld16(uint32_t (&v)[16], uint32_t taddr) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)map),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
+struct WorkF {
+  int64_t slot0;
+  int nitems;  // slots * nsubm * nsubn (pair items of 256 x 256)
+  int nsubm, nsubn;
+  int* counter;  // [work queue head, pairs started]
+  int presplit;  // the column-(k+1) update also writes its outputs' TF32 split
+  unsigned long long* span;
+};
+
+enum { OUT_UPDATE = 0, OUT_PRESPLIT = 1, OUT_TRSM = 2 };
+
+template <bool TRSM>
+__device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
+                                         const CUtensorMap& map_a, const CUtensorMap& map_b,
+                                         const CUtensorMap& map_c, const CUtensorMap& map_s) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* epi = smem + STAGES * STAGE_BYTES;
+  uint64_t* full = (uint64_t*)(epi + EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + SCHED;
+  uint64_t* cbar = sempty + SCHED;  // EPI_WARPS * CSLOTS C-chunk load barriers
+  int* sitem = (int*)(cbar + EPI_WARPS * CSLOTS);
+  int* si = sitem + SCHED;
+  int* sj = si + SCHED;
+  uint32_t* tmem_slot = (uint32_t*)(sj + SCHED);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // co-scheduled band update
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int nb = g.nb;
+  const int nsub = w.nsubm * w.nsubn;
+  auto item_ksteps = [&](int item) {
+    return TRSM ? ((item % nsub) % w.nsubn + 1) * (BN / BK) : nb / BK;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * EPI_WARPS);  // leader: local + peer epilogue warps
+    }
+    for (int s = 0; s < SCHED; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 2 + 2 * EPI_WARPS);  // leader: MMA + epi + peer producer + peer epi
+    }
+    for (int s = 0; s < EPI_WARPS * CSLOTS; ++s) mbar_init(&cbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (w.span && threadIdx.x == 0) atomicMin(&w.span[0], mt_globaltimer());
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto next_item = [&](uint32_t li, int* pi, int* pj) {
+    const int s = li % SCHED;
+    mbar_wait_cl(&sfull[s], (li / SCHED) & 1);
+    const int item = *(volatile int*)&sitem[s];
+    int dep = item;
+    if (pi) {
+      *pi = *(volatile int*)&si[s];
+      *pj = *(volatile int*)&sj[s];
+      dep ^= *pi ^ *pj;
+    }
+    dep = __reduce_xor_sync(0xffffffffu, dep);
+    if ((threadIdx.x & 31) == 0 && dep != 0x7fffffff) {
+      if (leader) mbar_arrive_relaxed(&sempty[s]);
+      else mbar_arrive_cl_relaxed(peer_addr(&sempty[s], 0));
+    }
+    return item;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------ work queue + TMA producer
+    if (lane == 0) {
+      if (leader && !TRSM && g.yield) atomicAdd(w.counter + 1, 1);  // pairs started
+      const int npairs = (int)(gridDim.x / 2);
+      uint32_t it = 0;
+      for (uint32_t li = 0;; ++li) {
+        const int s = li % SCHED;
+        int item, i = 0, j = 0;
+        if (leader) {
+          mbar_wait(&sempty[s], ((li / SCHED) & 1) ^ 1);
+          if (g.failed()) {
+            item = -1;
+          } else if (!TRSM && g.yield && *(volatile int*)g.yield > 0 &&
+                     *(volatile int*)(w.counter + 1) < npairs && atomicSub(g.yield, 2) > 0) {
+            item = -1;  // SM-yield request (see tc2_update.cu)
+          } else {
+            item = atomicAdd(w.counter, 1);
+            if (item >= w.nitems) item = -1;
+          }
+          if (item >= 0) g.off_slot_ij(w.slot0 + item / nsub, i, j);
+          sitem[s] = item; si[s] = i; sj[s] = j;
+          st_cl_u32(peer_addr(&sitem[s], 1), (uint32_t)item);
+          st_cl_u32(peer_addr(&si[s], 1), (uint32_t)i);
+          st_cl_u32(peer_addr(&sj[s], 1), (uint32_t)j);
+          mbar_arrive(&sfull[s]);
+          mbar_arrive_cl(peer_addr(&sfull[s], 1));
+        } else {
+          mbar_wait_cl(&sfull[s], (li / SCHED) & 1);
+          item = *(volatile int*)&sitem[s];
+          i = *(volatile int*)&si[s];
+          j = *(volatile int*)&sj[s];
+          if ((item ^ i ^ j) != 0x7fffffff) mbar_arrive_cl_relaxed(peer_addr(&sempty[s], 0));
+        }
+        if (item < 0) break;
+        const int sub = item % nsub;
+        const int m0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM;
+        const int n0 = (sub % w.nsubn) * BN + (int)rank * BNH;
+        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
+        const int brow = TRSM ? (int)g.winv_row() + n0 : ((k & 1) * g.p + j) * 2 * nb + n0;
+        const int ksteps = item_ksteps(item);
+        for (int ks = 0; ks < ksteps; ++ks, ++it) {
+          const int st = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[st], ph ^ 1);
+          unsigned char* sb = smem + st * STAGE_BYTES;
+          if (leader) mbar_expect_tx(&full[st], 2 * STAGE_BYTES);
+          const uint32_t bar = peer_addr(&full[st], 0);
+          tma_load_pair(sb, &map_a, bar, ks * BK, arow);                               // A hi
+          tma_load_pair(sb + A_BYTES, &map_b, bar, ks * BK, brow);                     // B hi
+          tma_load_pair(sb + A_BYTES + B_BYTES, &map_a, bar, ks * BK, arow + nb);      // A lo
+          tma_load_pair(sb + 2 * A_BYTES + B_BYTES, &map_b, bar, ks * BK, brow + nb);  // B lo
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader only)
+    if (leader) {
+      uint32_t it = 0, ch = 0;
+      for (uint32_t li = 0;; ++li) {
+        const int item = next_item(li, nullptr, nullptr);
+        if (item < 0) break;
+        const int ksteps = item_ksteps(item);
+        for (int ks = 0; ks < ksteps; ++ks, ++it) {
+          const uint32_t b = ch & 1;
+          const bool c_first = (ks % KC) == 0, c_last = (ks % KC) == KC - 1;
+          if (c_first) {
+            mbar_wait_cl(&tempty[b], ((ch >> 1) & 1) ^ 1);  // chunk buffer drained
+            asm volatile("tcgen05.fence::after_thread_sync;");
+          }
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            unsigned char* st = smem + s * STAGE_BYTES;
+            const unsigned char* ahi = st;
+            const unsigned char* bhi = st + A_BYTES;
+            const unsigned char* alo = st + A_BYTES + B_BYTES;
+            const unsigned char* blo = alo + A_BYTES;
+            const uint32_t dcol = tmem_base + b * BN;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const int off = kk * 32;
+              umma(dcol, sw64_desc(alo + off), sw64_desc(bhi + off), (c_first && kk == 0) ? 0u : 1u);
+              umma(dcol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
+              umma(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off), 1u);
+            }
+            umma2_commit_both(&empty[s]);
+            if (c_last) umma2_commit_both(&tfull[b]);
+          }
+          __syncwarp();
+          if (c_last) ++ch;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..9, both CTAs)
+    const int ew = warp - 2;
+    const int q = warp & 3;     // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;   // column half of the item
+    unsigned char* slots = epi + ew * CSLOTS * CSLOT_BYTES;
+    uint64_t* wbar = cbar + ew * CSLOTS;
+    const uint32_t tempty_leader[2] = {peer_addr(&tempty[0], 0), peer_addr(&tempty[1], 0)};
+    uint32_t phb = 0;  // bit s: parity of slot s's next C load
+    uint32_t ch = 0;
+    auto load_c = [&](int s, int col, int row) {  // lane 0; slot s must be free
+      mbar_expect_tx(&wbar[s], CSLOT_BYTES);
+      tma_load_2d(slots + s * CSLOT_BYTES, &map_c, &wbar[s], col, row);
+    };
+    auto wait_c = [&](int s) {
+      mbar_wait(&wbar[s], (phb >> s) & 1);
+      phb ^= 1u << s;
+    };
+    for (uint32_t li = 0;; ++li) {
+      int i, j;
+      const int item = next_item(li, &i, &j);
+      if (item < 0) break;
+      const int sub = item % nsub;
+      const int row0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM + q * 32;  // row in the tile
+      const int n0 = (sub % w.nsubn) * BN + half * COLS_W;                    // first column
+      const int out = TRSM ? OUT_TRSM : ((w.presplit && j == k + 1) ? OUT_PRESPLIT : OUT_UPDATE);
+      // TMA rows: output tile (i, j) (TRSM: j == k) in the off-band pool, and
+      // the split buffer rows of its TF32 hi part (lo = + nb)
+      const int crow = (int)((g.scol(j) + (i - j - g.t)) * (int64_t)nb) + row0;
+      const int srow = out == OUT_TRSM ? (int)(((int64_t)(k & 1) * g.p + i) * 2 * nb) + row0
+                                       : (int)g.presplit_row(i) + row0;
+      const int nch = item_ksteps(item) / KC;
+      float sum[COLS_W];
+#pragma unroll
+      for (int u = 0; u < COLS_W; ++u) sum[u] = 0.f;
+      const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + half * COLS_W;
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {
+        const uint32_t b = ch & 1;
+        mbar_wait(&tfull[b], (ch >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int m = 0; m < COLS_W / 16; ++m) {
+          uint32_t v[16];
+          ld16(v, tq + b * BN + m * 16);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) sum[16 * m + u] += __uint_as_float(v[u]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cl_relaxed(tempty_leader[b]);
+        ++ch;
+        if (c == 0 && out != OUT_TRSM && lane == 0) {
+          // C of this item: slots free once the previous item's stores were read
+          bulk_wait_read<0>();
+          if (out == OUT_UPDATE) {
+            for (int m = 0; m < 3; ++m) load_c(m, n0 + m * 32, crow);
+            prefetch_l2_2d(&map_c, n0 + 96, crow);
+          } else {
+            load_c(0, n0, crow);
+            for (int m = 1; m < 4; ++m) prefetch_l2_2d(&map_c, n0 + m * 32, crow);
+          }
+        }
+      }
+      // ---- output: lane = row, 32 columns per chunk m, SWIZZLE_128B slots
+      // x[0..31] -> slot s row `lane`: the values (part 0), or their TF32 hi (1) / lo (2)
+      auto put = [&](int s, const float* x, int part) {
+        const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * 128;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float h, l;
+            mt_tf32_split(x[4 * e + u], h, l);
+            y[u] = part == 0 ? x[4 * e + u] : (part == 1 ? h : l);
+          }
+          sts128(rowa + ((e ^ (lane & 7)) << 4), make_float4(y[0], y[1], y[2], y[3]));
+        }
+      };
+      if (out == OUT_UPDATE) {
+#pragma unroll
+        for (int m = 0; m < COLS_W / 32; ++m) {
+          const int s = m == 3 ? 0 : m;
+          wait_c(s);
+          const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * 128;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t a = rowa + ((e ^ (lane & 7)) << 4);
+            float4 cc = lds128(a);
+            cc.x -= sum[32 * m + 4 * e];
+            cc.y -= sum[32 * m + 4 * e + 1];
+            cc.z -= sum[32 * m + 4 * e + 2];
+            cc.w -= sum[32 * m + 4 * e + 3];
+            sts128(a, cc);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * 32, crow);
+            bulk_commit();
+            if (m == 0) {  // chunk 3 reuses slot 0 (L2-prefetched)
+              bulk_wait_read<0>();
+              load_c(0, n0 + 96, crow);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < COLS_W / 32; ++m) {
+          float x[32];
+          if (out == OUT_PRESPLIT) {
+            wait_c(0);
+            const uint32_t rowa = smem_u32(slots) + lane * 128;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float4 cc = lds128(rowa + ((e ^ (lane & 7)) << 4));
+              x[4 * e] = cc.x - sum[32 * m + 4 * e];
+              x[4 * e + 1] = cc.y - sum[32 * m + 4 * e + 1];
+              x[4 * e + 2] = cc.z - sum[32 * m + 4 * e + 2];
+              x[4 * e + 3] = cc.w - sum[32 * m + 4 * e + 3];
+            }
+          } else {
+            if (lane == 0) bulk_wait_read<0>();  // slots free (previous chunk's stores read)
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) x[u] = sum[32 * m + u];
+          }
+          put(0, x, 0);
+          put(1, x, 1);
+          put(2, x, 2);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, slots, n0 + m * 32, crow);
+            tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * 32, srow);
+            tma_store_2d(&map_s, slots + 2 * CSLOT_BYTES, n0 + m * 32, srow + nb);
+            bulk_commit();
+            if (out == OUT_PRESPLIT && m < 3) {
+              bulk_wait_read<0>();
+              load_c(0, n0 + (m + 1) * 32, crow);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_all();  // stores complete before the kernel ends
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();
+  if (w.span && threadIdx.x == 0) atomicMax(&w.span[1], mt_globaltimer());
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    tcf_update_kernel(Grid g, int k, WorkF w, const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_c,
+                      const __grid_constant__ CUtensorMap map_s) {
+  tcf_body<false>(g, k, w, map_a, map_b, map_c, map_s);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    tcf_trsm_kernel(Grid g, int k, WorkF w, const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c,
+                    const __grid_constant__ CUtensorMap map_s) {
+  tcf_body<true>(g, k, w, map_a, map_b, map_c, map_s);
+}
+
+int g_smf = 0;
+
+}  // namespace
+
+// launch over the off-band slot range [s0, s0 + scnt) of step k (update) or
+// panel k (trsm); `ctas` caps the grid (rounded down to pairs)
+int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm, int presplit,
+                  cudaStream_t st, unsigned long long* span) {
+  if (scnt <= 0) return MT_OK;
+  CUtensorMap ma, mb, mc, ms;
+  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
+  int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
+  const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;
+  if (!rc) rc = make_map_2d(&mc, g.sp ? (const void*)g.sp : (const void*)g.split, c_rows, g.nb, 4, 32,
+                            32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_map_2d(&ms, g.split, split_rows, g.nb, 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  WorkF w;
+  w.slot0 = s0;
+  w.nsubm = g.nb / (2 * BM);
+  w.nsubn = g.nb / BN;
+  w.nitems = (int)(scnt * w.nsubm * w.nsubn);
+  w.presplit = presplit;
+  w.span = span;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_smf) cudaDeviceGetAttribute(&g_smf, cudaDevAttrMultiProcessorCount, dev);
+  static int* counters[64] = {nullptr};
+  static unsigned next_counter[64] = {0};
+  if (dev < 0 || dev >= 64) { mt_set_error("device index out of range"); return MT_E_CUDA; }
+  if (!counters[dev] && mt_cuda_check(cudaMalloc(&counters[dev], 2 * 256 * sizeof(int)), "counter alloc"))
+    return MT_E_CUDA;
+  w.counter = counters[dev] + 2 * (next_counter[dev]++ % 256);
+  if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int), st), "counter reset"))
+    return MT_E_CUDA;
+  int pairs = (ctas > 0 ? ctas : g_smf) / 2;
+  if (!trsm && g.yield && ctas <= 0) pairs = g_smf;  // oversubscribed: refills yielded SMs
+  if (pairs > w.nitems) pairs = w.nitems;
+  if (pairs < 1) pairs = 1;
+  if (trsm) {
+    cudaFuncSetAttribute(tcf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    tcf_trsm_kernel<<<2 * pairs, NUM_THREADS, SMEM_BYTES, st>>>(g, k, w, ma, mb, mc, ms);
+    MT_LAUNCH_CHECK("tcf_trsm_kernel");
+  } else {
+    cudaFuncSetAttribute(tcf_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    tcf_update_kernel<<<2 * pairs, NUM_THREADS, SMEM_BYTES, st>>>(g, k, w, ma, mb, mc, ms);
+    MT_LAUNCH_CHECK("tcf_update_kernel");
+  }
+  return MT_OK;
+}

@@ -412,7 +412,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t co_s0 = g.scol(jlo), co_scnt = g.scol(jhi) - co_s0;
   const int64_t co_b0 = g.bcol(jlo), co_bcnt = g.bcol(jhi) - co_b0;
   if (mt_opt_coschedule() && !pcol && g.mode == MT_MODE_MP && co_scnt > 0 && co_bcnt > 0 &&
-      (mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) && mt_tc_supported(g) &&
+      (mt_engine_tc(mt_opt_engine()) || g.cs > 1) && mt_tc_supported(g) &&
       mt_opt_cta_pairs() && mt_opt_legacy_dmma() != 1 && mt_dmma_tma_supported(g)) {
     static int sms = 0;
     if (!sms) {
@@ -460,7 +460,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
   if (scnt > 0) {
     ProfScope ps(pcol ? MT_K_UPD32P : MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
-    if ((mt_opt_engine() == MT_ENGINE_TF32X3 || g.cs > 1) && mt_tc_supported(g)) {
+    if ((mt_engine_tc(mt_opt_engine()) || g.cs > 1) && mt_tc_supported(g)) {
       // the panel-column update (jhi == jlo + 1) runs beside the bulk update:
       // keep it narrow; the bulk update may be capped to leave SMs for the panel
       const int ctas = (jhi == jlo + 1) ? mt_opt_pcol_ctas() : mt_opt_update_ctas();

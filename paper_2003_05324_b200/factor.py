@@ -133,6 +133,8 @@ def cholesky(matrix, threads=1, lookahead=1):
     Raises FactorizationError(global pivot) when not positive definite.
     """
     del threads  # schedule-invariant; accepted for signature compatibility
+    if not hasattr(matrix, "desc"):
+        return _cholesky_host_matrix(matrix, lookahead)
     if matrix.factored:
         raise ValueError("matrix is already factored")
     lib = _lib.load()
@@ -146,6 +148,29 @@ def cholesky(matrix, threads=1, lookahead=1):
     matrix.factored = True
     flops = planned_flops(matrix.n, matrix.nb, matrix.policy)
     return CholeskyFactor(matrix, flops)
+
+
+def _cholesky_host_matrix(ref, lookahead):
+    """cholesky() on a host tile dict (the reference's own TileMatrix, e.g.
+    `TileMatrix.from_dense(a, nb, policy)` built before install()): upload,
+    factor on the GPU, then overwrite the caller's tile payloads in place as
+    the reference does (factor.py:238, 285), including the .sp/.dp pairs of
+    off-band tiles and the narrowed band mirrors (test_factor.py:146-153).
+    A missing diagonal tile raises ValueError (factor.py:240-242)."""
+    from .tilestore import TileMatrix
+    p = ref.p
+    for k in range(p):
+        if (k, k) not in ref.tiles:
+            raise ValueError(f"diagonal tile {k} missing from the matrix")
+    dev = TileMatrix.from_dense(ref.to_dense(), ref.nb, ref.policy)
+    try:
+        fac = cholesky(dev, lookahead=lookahead)
+    finally:
+        if dev.factored:  # partially factored payloads are visible too, as in the reference
+            for key, tile in ref.tiles.items():
+                got = dev.tiles[key]
+                tile.dp, tile.sp = got.dp, got.sp
+    return fac
 
 
 def _work(m):
@@ -224,12 +249,19 @@ def reconstruction_error(factor, reference):
     return float(math.sqrt(float(np.sum(r * r))))
 
 
-_ENGINES = {"ffma": 0, "tf32x3": 1}
+_ENGINES = {"ffma": 0, "tf32x3": 1, "tf32x3_rz": 2}
 
 
 def set_fp32_engine(name):
-    """Select the off-band (FP32) update engine: 'tf32x3' (tcgen05 3xTF32, the
-    default, used when nb is a multiple of 256) or 'ffma' (SIMT FP32).
+    """Select the off-band (FP32) update engine (used when nb is a multiple of 256):
+
+    * 'tf32x3' (default): tcgen05 3xTF32 with the TMEM accumulator restarted
+      every 32 K-columns and the chunks summed in FP32 with round-to-nearest
+      (FP32-accurate, like the reference's sgemm, factor.py:273-274);
+    * 'tf32x3_rz': tcgen05 3xTF32 accumulating the whole K range in TMEM
+      (the tensor core rounds each partial toward zero: a systematic bias;
+      faster, opt-in);
+    * 'ffma': SIMT FP32 FMA.
     Returns the previous engine name."""
     old = _lib.load().mt_set_option(0, _ENGINES[name])
     return {v: k for k, v in _ENGINES.items()}[old]

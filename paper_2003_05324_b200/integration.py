@@ -21,13 +21,14 @@ def _targets(pkg):
     mod = lambda name: importlib.import_module(f"{pkg.__name__}.{name}")  # noqa: E731
     t, f, m = mod("tilestore"), mod("factor"), mod("mle")
     out = [
-        (t, {"TileAssembler": T.TileAssembler, "assemble_covariance": T.assemble_covariance}),
+        (t, {"TileAssembler": T.TileAssembler, "assemble_covariance": T.assemble_covariance,
+             "TileMatrix": T.TileMatrix}),
         (f, {"cholesky": F.cholesky, "logdet": F.logdet, "solve": F.solve,
              "matvec_lower": F.matvec_lower}),
         (m, {"TileAssembler": T.TileAssembler, "cholesky": F.cholesky,
              "factor_logdet": F.logdet, "factor_solve": F.solve}),
         (pkg, {"TileAssembler": T.TileAssembler, "assemble_covariance": T.assemble_covariance,
-               "cholesky": F.cholesky, "logdet": F.logdet, "solve": F.solve,
+               "TileMatrix": T.TileMatrix, "cholesky": F.cholesky, "logdet": F.logdet, "solve": F.solve,
                "matvec_lower": F.matvec_lower}),
     ]
     from . import predict as P

@@ -68,10 +68,7 @@ def test_krige_vs_oracle_larger(gpu):
     assert np.max(np.abs(got_dp - want_dp)) <= 1e-8 * scale
     # MP t=2, same band as the reference.  The SIMT FFMA engine (round-to-nearest
     # FP32, like OpenBLAS sgemm) must be as close to the exact (DP) prediction as
-    # the reference's own MP (within 2x of its gap).  The tcgen05 3xTF32 engine
-    # accumulates in TMEM with round-toward-zero; that systematic bias moves the
-    # (ill-conditioned) kriging weights ~7-12x further than the reference's MP
-    # (reproduced on the CPU by tools/emulate_tf32x3.py), bounded here at 16x.
+    # the reference's own MP (within 2x of its gap).
     want_mp = O.krige(locs, z, test, th, nb, "mp", 2)
     gap = max(np.max(np.abs(want_mp - want_dp)), 1e-9 * scale)
     pol = mt.PrecisionPolicy.mp(diag_thick=2)
@@ -81,8 +78,17 @@ def test_krige_vs_oracle_larger(gpu):
     finally:
         mt.set_fp32_engine(old)
     assert np.max(np.abs(got_ff - want_dp)) <= 2.0 * gap, (np.max(np.abs(got_ff - want_dp)), gap)
+    # default tcgen05 engine (round-to-nearest chunk accumulation): the same 2x
+    # bound as FFMA (measured 1.49x).  The opt-in whole-K engine (TMEM adds round
+    # toward zero) sits ~8x out (tools/emulate_flush.py reproduces both on CPU)
     got_tc = mt.krige(ds, test, mt.MaternParams(*th), nb, pol)
-    assert np.max(np.abs(got_tc - want_dp)) <= 16.0 * gap, (np.max(np.abs(got_tc - want_dp)), gap)
+    assert np.max(np.abs(got_tc - want_dp)) <= 2.0 * gap, (np.max(np.abs(got_tc - want_dp)), gap)
+    old = mt.set_fp32_engine("tf32x3_rz")
+    try:
+        got_rz = mt.krige(ds, test, mt.MaternParams(*th), nb, pol)
+    finally:
+        mt.set_fp32_engine(old)
+    assert np.max(np.abs(got_rz - want_dp)) <= 16.0 * gap
 
 
 def test_krige_properties(gpu):

@@ -21,6 +21,16 @@ def _mt():
 
 
 @pytest.fixture
+def rz_engine(gpu):
+    """The opt-in whole-K TMEM engine: its kernel variants (single CTA, CTA
+    pairs, 256 x 512 items) apply identical MMA sequences and must agree bitwise."""
+    mt = _mt()
+    old = mt.set_fp32_engine("tf32x3_rz")
+    yield mt
+    mt.set_fp32_engine(old)
+
+
+@pytest.fixture
 def engine(gpu):
     mt = _mt()
     old = mt.set_fp32_engine("tf32x3")
@@ -49,7 +59,11 @@ def test_tf32x3_factor_accuracy_vs_ffma_and_oracle(engine):
         err_tc = max(err_tc, float(np.max(np.abs(f_tc.tiles[key].dp - dp))))
         err_ff = max(err_ff, float(np.max(np.abs(f_ff.tiles[key].dp - dp))))
     assert err_ff < 5e-5 and err_tc < 5e-5, (err_tc, err_ff)
-    assert err_tc <= 8.0 * err_ff + 1e-7, (err_tc, err_ff)
+    # FP32 accuracy gate (north_star: 3xTF32 only if it matches FP32): the
+    # default engine restarts the TMEM accumulation every 32 K-columns and sums
+    # the chunks with round-to-nearest (tcf_update.cu); measured on B200 at
+    # 0.27x the round-to-nearest FFMA engine's distance from the reference factor
+    assert err_tc <= 1.5 * err_ff, (err_tc, err_ff)
     # band tiles of rows k < t are untouched by FP32 work: equal across engines
     assert np.array_equal(f_tc.tiles[(0, 0)].dp, f_ff.tiles[(0, 0)].dp)
 
@@ -189,7 +203,7 @@ def test_sm_yield_keeps_results_bitwise(gpu, ysms):
 
 
 @pytest.mark.parametrize("n,nb,t,ysms", [(4096, 256, 2, 0), (6144, 512, 3, 32), (3000, 256, 1, 200)])
-def test_cta_pair_kernel_bitwise_equals_single_cta(gpu, n, nb, t, ysms):
+def test_cta_pair_kernel_bitwise_equals_single_cta(rz_engine, n, nb, t, ysms):
     """The CTA-pair (tcgen05.mma.cta_group::2, M=256) FP32 update and off-band
     TRSM apply the same MMA sequence to every output element as the
     single-CTA kernel: factors are bit-identical (option 9), with and without
@@ -240,7 +254,7 @@ def test_coscheduled_band_update_bitwise(gpu, n, nb, t):
 
 
 @pytest.mark.parametrize("n,t,co", [(8192, 3, 1), (7000, 2, 0), (12288, 8, 1)])
-def test_wide_pair_items_bitwise(gpu, n, t, co):
+def test_wide_pair_items_bitwise(rz_engine, n, t, co):
     """Option 12 (bulk update on 256 x 512 CTA-pair items, single-buffered TMEM)
     applies the same MMA sequence per output element: bitwise equal to the
     256 x 256-item kernel, with and without co-scheduling, ragged last tile."""
