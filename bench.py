@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dp", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    if os.environ.get("MT_BENCH_ARGV") is not None and "WORLD_SIZE" in os.environ:
+        return ap.parse_args(json.loads(os.environ["MT_BENCH_ARGV"]))  # spawned by --gpus N
     return ap.parse_args()
 
 
@@ -598,10 +600,12 @@ def spawn_ranks(args):
     """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks
     (one process per GPU) with torch.distributed.run on 127.0.0.1 and return
     its exit code.  Rank 0 prints the JSON line."""
+    # the script's own flags travel in the environment: torchrun's parser would
+    # claim abbreviations such as --n (--nnodes) or --t (--tee)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
-           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd, env=dict(os.environ))
+           f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    return subprocess.call(cmd, env=dict(os.environ, MT_BENCH_ARGV=json.dumps(sys.argv[1:])))
 
 
 def nccl_debug_env():

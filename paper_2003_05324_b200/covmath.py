@@ -72,8 +72,11 @@ class DistanceMetric:
         return _lib.METRIC_CODE[self.kind]
 
 
-def matern_array(r, params):
-    """Matern covariance at distances r, evaluated on the GPU (covmath.py:261-283)."""
+def matern_array(r, params, use_closed_forms=True):
+    """Matern covariance at distances r, evaluated on the GPU (covmath.py:261-283).
+
+    use_closed_forms=False forces the general Bessel route even at nu = 1/2
+    and 3/2 (the reference's switch for exercising the Bessel machinery)."""
     torch = _lib.require_cuda()
     r = np.asarray(r, dtype=np.float64)
     if r.size and np.min(r) < 0.0:
@@ -82,6 +85,8 @@ def matern_array(r, params):
     d_r = torch.from_numpy(flat).cuda()
     d_out = torch.empty_like(d_r)
     th = _lib.matern_struct(*params.as_tuple())
+    if not use_closed_forms:
+        th.kind = 2  # Bessel route; its constants are prepared for every nu
     _lib.check(_lib.load().mt_matern_array(_lib.ptr(d_r), flat.size, th, _lib.ptr(d_out),
                                            _lib.stream_handle()), "mt_matern_array")
     return d_out.cpu().numpy().reshape(r.shape)

@@ -157,3 +157,41 @@ def test_generation_large_grid_sample_vs_oracle(gpu):
             np.testing.assert_allclose(t.dp, blk, rtol=1e-13, atol=0)
         else:
             assert np.mean(t.sp == blk.astype(np.float32)) > 0.9999
+
+
+@pytest.mark.parametrize("name,seed,nb", [("config1", 0, 256), ("strong1024", 3, 128),
+                                          ("ragged1000", 4, 96)])
+def test_generate_field_matches_reference(gpu, name, seed, nb):
+    """geodata.generate_field (geodata.py:88-106) on the GPU -- full-DP factor of
+    the Matern covariance times v = default_rng(seed).standard_normal(n) --
+    against the field the reference itself drew for the golden (same recipe:
+    tests/golden/make_golden.py `_sim`, then morton_sort)."""
+    import paper_2003_05324_b200 as mt
+    g = load_golden(name)
+    n = len(g["z"])
+    th = mt.MaternParams(*(float(v) for v in g["theta"]))
+    locs = mt.generate_locations(n, seed=mt.derive_seed(seed, 0))
+    ds, _ = mt.morton_sort(mt.generate_field(locs, th, seed=mt.derive_seed(seed, 1), nb=nb))
+    assert np.array_equal(ds.locations, g["locs"])
+    # the two DP factors differ only by FP64 summation order (DMMA vs OpenBLAS)
+    err = float(np.max(np.abs(ds.z - g["z"]))) / float(np.max(np.abs(g["z"])))
+    print(f"generate_field {name}: max |dz| / max |z| = {err:.3e}")
+    assert err <= 1e-8, err
+
+
+def test_matern_general_path_matches_closed_forms(gpu):
+    """covmath.matern_array(..., use_closed_forms=False) forces the Bessel route
+    at nu = 1/2 and 3/2 (reference test_covmath.py:139-150, same draws)."""
+    import paper_2003_05324_b200 as mt
+    rng = np.random.default_rng(5)
+    for smoothness in (0.5, 1.5):
+        variance = float(rng.uniform(0.1, 5.0))
+        spatial_range = float(rng.uniform(0.01, 2.0))
+        p = mt.MaternParams(variance, spatial_range, smoothness)
+        r = 10.0 ** rng.uniform(-5, 1, size=500) * spatial_range
+        got = mt.matern_array(r, p, use_closed_forms=False)
+        z = r / spatial_range
+        ref = variance * np.exp(-z) * (1.0 if smoothness == 0.5 else 1.0 + z)
+        assert np.allclose(got, ref, rtol=1e-10, atol=0.0)
+        # the default route uses the closed form
+        assert np.allclose(mt.matern_array(r, p), ref, rtol=1e-13, atol=0.0)

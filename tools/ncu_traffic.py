@@ -38,6 +38,10 @@ def summarise(path):
         # grid; the co-scheduled tc2w bulk kernel has a per-step grid, keep it whole
         if "launch__grid_size" in ms and names[lid].startswith("tc2_update_kernel"):
             names[lid] += f"[grid={int(ms['launch__grid_size'])}]"
+        # tcf_update_kernel: panel-column updates run on 64 CTAs (option 4), the
+        # co-scheduled bulk updates on a per-step grid > 64
+        elif "launch__grid_size" in ms and names[lid].startswith("tcf_update_kernel"):
+            names[lid] += "[pcol]" if int(ms["launch__grid_size"]) <= 64 else "[bulk]"
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for lid, ms in per.items():
         a = agg[names[lid]]
