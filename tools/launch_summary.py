@@ -14,6 +14,8 @@ def summarise(path):
     scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3,
              "s": 1e6, "second": 1e6}
     for d in data:
+        if d.get("Metric Name", "gpu__time_duration.sum") != "gpu__time_duration.sum":
+            continue
         m = re.search(r"(\w+_kernel(?:<[^>]*>)?|\w*elementwise\w*)", d["Kernel Name"])
         name = m.group(1) if m else d["Kernel Name"][:40]
         agg[name][0] += 1
