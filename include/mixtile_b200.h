@@ -54,10 +54,12 @@ extern "C" {
  *   status:  int64[4] device: [0] first failing global pivot (-1 = none),
  *            [1] FP32 narrowing overflow count, [2] duplicate-location pairs.
  *   split:   TF32 hi/lo split of panels k (ring of 2): tile (i, k) of panel k at
- *            split + ((k&1)*p + i)*2*nb*nb (hi) and + nb*nb (lo); then the
+ *            split + ((k&1)*pr + ring(i))*2*nb*nb (hi) and + nb*nb (lo), pr = p
+ *            and ring(i) = i on one GPU (see row_stride below); then the
  *            pre-TRSM split of the next panel's off-band tiles at
- *            split + (4p + 2i)*nb*nb, and the split of W = L_kk^{-1} (row-major)
- *            at split + 6p*nb*nb (hi) / + nb*nb (lo): 6p + 2 tiles in all.
+ *            split + (4pr + 2i)*nb*nb, and the split of W = L_kk^{-1} (row-major)
+ *            at split + (4pr + 2p)*nb*nb (hi) / + nb*nb (lo): 6p + 2 tiles on
+ *            one GPU (mt_split_tiles), mt_split_tiles_ex() on a P x Q grid.
  */
 typedef struct mt_tiles {
   int64_t n;
@@ -72,14 +74,20 @@ typedef struct mt_tiles {
   float* split;  /* optional (MP, tensor-core engine): mt_split_tiles() FP32 tiles holding
                     the TF32 hi/lo split of the two panels in flight; NULL disables the
                     tcgen05 3xTF32 update (FFMA fallback kernel is used instead) */
-  /* multi-GPU (tile-column-cyclic 1 x g grid): this rank stores only tile
-   * columns j = col_offset + m * col_stride, in the same per-column pool order;
-   * col_stride = 1, col_offset = 0 is the single-GPU layout.  dpanel:
-   * mt_dpanel_tiles() FP64 tiles receiving the band rows of the panels in
-   * flight (NULL on a single GPU). */
+  /* multi-GPU, 2D block-cyclic over a P x Q process grid: this rank stores
+   * only the tiles (i, j) with j = col_offset (mod col_stride = Q) and
+   * i = row_offset (mod row_stride = P), column by column, rows ascending;
+   * strides 1 and offsets 0 are the single-GPU layout.  dpanel:
+   * mt_dpanel_tiles_ex() FP64 tiles receiving the FP64 rows of the two panels
+   * in flight (NULL on a single GPU).  Panel rings (split, dpanel) are in
+   * "ring order" on a multi-GPU grid: tile row i at position
+   * (i mod L) * ceil(p / L) + i / L, L = lcm(P, Q) (L = 1 when P = 1), so the
+   * rows one process row or column receives are contiguous. */
   int32_t col_stride;
   int32_t col_offset;
   double* dpanel;
+  int32_t row_stride;
+  int32_t row_offset;
 } mt_tiles;
 
 /* Matern parameters + per-theta Bessel constants (covmath.py:72-95, 228-283),
@@ -173,13 +181,23 @@ int mt_evaluate(const mt_tiles* g, const double* locs, int32_t metric, double ra
                 const mt_matern* theta, const double* z, double* work, double* out2,
                 int32_t lookahead, void* stream);
 
-/* ---- multi-GPU factorization, one process per GPU (tile-column-cyclic layout,
- * col_stride = #ranks, col_offset = rank).  The host drives the step loop and
- * broadcasts each panel (split hi/lo rows k+1.. of panel k and the FP64 band
- * rows in dpanel) from the column owner; every tile keeps the single-GPU
- * update order, so the factor is bitwise identical for any rank count. */
-/* POTRF(k) + TRSM(k) of the owned tile column k (factor.py:249-265). */
+/* ---- multi-GPU factorization, one process per GPU, 2D block-cyclic over a
+ * P x Q grid (row_stride = P, col_stride = Q; rank (r, c) stores tiles with
+ * i = r mod P, j = c mod Q).  The host drives the step loop: POTRF(k) on the
+ * owner of (k, k); on P > 1 L_kk, its 32x32 inverses and W = L_kk^{-1}
+ * (mt_diag_regions) go down process column k mod Q; TRSM(k) on that column's
+ * ranks; panel k's rows (split hi/lo + FP64 rows in dpanel, ring order) are
+ * broadcast along process rows, then down process columns.  Every tile keeps
+ * the single-GPU update order: the factor is bitwise identical for any grid. */
+/* POTRF(k) + TRSM(k) of the owned tile column k on a 1 x Q grid (factor.py:249-265). */
 int mt_panel(const mt_tiles* g, int32_t k, void* stream);
+/* POTRF(k) on the owner of (k, k) (+ L_kk into dpanel, W split, on a grid). */
+int mt_panel_factor(const mt_tiles* g, int32_t k, void* stream);
+/* TRSM(k) of this rank's rows of tile column k. */
+int mt_panel_solve(const mt_tiles* g, int32_t k, void* stream);
+/* {offset, count} of L_kk in dpanel (doubles), of its 32x32 inverses in scratch
+ * (floats) and of W's split in split (floats): the column broadcast of panel k. */
+int mt_diag_regions(const mt_tiles* g, int32_t k, int64_t* out6);
 /* Step-k trailing updates of the owned columns in [jlo, jhi) (factor.py:266-274);
  * panel k must be present in split/dpanel. */
 int mt_update(const mt_tiles* g, int32_t k, int32_t jlo, int32_t jhi, void* stream);
@@ -196,13 +214,24 @@ int mt_yield_request(int32_t sms, void* stream);
 int mt_logdet_partials(const mt_tiles* g, double* partial, void* stream);
 /* Forward-sweep step i on the owner of column i: y_i = L_ii^{-1} x_i, x_r -= L_ri y_i. */
 int mt_fwd_step(const mt_tiles* g, int32_t i, double* x, void* stream);
+/* The same split by owner: which bit 0 = y_i = L_ii^{-1} x_i (owner of (i, i)),
+ * bit 1 = x_r -= L_ri y_i for this rank's rows r > i (ranks of column i). */
+int mt_fwd_step_ex(const mt_tiles* g, int32_t i, int32_t which, double* x, void* stream);
 /* Sum of squares of m device doubles with mt_quad's fixed-order reduction
  * (work: >= 1024 device doubles) -> *out (device). */
 int mt_sumsq(const double* x, int64_t m, double* work, double* out, void* stream);
-/* Local pool sizes (tiles) of a rank's columns; dpanel ring size. */
+/* Local pool sizes (tiles) of a rank's columns (1 x Q grid); dpanel ring size. */
 int mt_local_tiles(int32_t p, int32_t t, int32_t mode, int32_t col_stride, int32_t col_offset,
                    int64_t* ndp, int64_t* nsp);
 int64_t mt_dpanel_tiles(int32_t p, int32_t t, int32_t mode);
+/* The same on a P x Q grid for rank (row_offset, col_offset); ring sizes. */
+int mt_local_tiles_ex(int32_t p, int32_t t, int32_t mode, int32_t row_stride, int32_t row_offset,
+                      int32_t col_stride, int32_t col_offset, int64_t* ndp, int64_t* nsp);
+int64_t mt_dpanel_tiles_ex(int32_t p, int32_t row_stride, int32_t col_stride);
+int64_t mt_split_tiles_ex(int32_t p, int32_t t, int32_t mode, int32_t row_stride,
+                          int32_t col_stride);
+/* Ring position of tile row i on a P x Q grid (see mt_tiles.row_stride). */
+int32_t mt_ring_pos(int32_t p, int32_t row_stride, int32_t col_stride, int32_t i);
 
 /* Synchronise `stream` and read status: *bad_pivot (-1 none), *overflow,
  * *duplicates.  Returns MT_E_NOT_SPD / MT_E_OVERFLOW when set, else MT_OK. */

@@ -34,6 +34,8 @@ class MtTiles(ctypes.Structure):
         ("col_stride", ctypes.c_int32),
         ("col_offset", ctypes.c_int32),
         ("dpanel", ctypes.c_void_p),
+        ("row_stride", ctypes.c_int32),
+        ("row_offset", ctypes.c_int32),
     ]
 
 
@@ -88,14 +90,23 @@ SIGNATURES = {
     "mt_put_tile": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V, _V]),
     "mt_set_option": (_I32, [_I32, _I32]),
     "mt_panel": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
+    "mt_panel_factor": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
+    "mt_panel_solve": (ctypes.c_int, [_P(MtTiles), _I32, _V]),
+    "mt_diag_regions": (ctypes.c_int, [_P(MtTiles), _I32, _P(_I64)]),
     "mt_update": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _V]),
     "mt_update_ex": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _I32, _I32, _V]),
     "mt_yield_request": (ctypes.c_int, [_I32, _V]),
     "mt_logdet_partials": (ctypes.c_int, [_P(MtTiles), _V, _V]),
     "mt_fwd_step": (ctypes.c_int, [_P(MtTiles), _I32, _V, _V]),
+    "mt_fwd_step_ex": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _V, _V]),
     "mt_sumsq": (ctypes.c_int, [_V, _I64, _V, _V, _V]),
     "mt_local_tiles": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _P(_I64), _P(_I64)]),
     "mt_dpanel_tiles": (_I64, [_I32, _I32, _I32]),
+    "mt_local_tiles_ex": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _I32, _P(_I64),
+                                         _P(_I64)]),
+    "mt_dpanel_tiles_ex": (_I64, [_I32, _I32, _I32]),
+    "mt_split_tiles_ex": (_I64, [_I32, _I32, _I32, _I32, _I32]),
+    "mt_ring_pos": (_I32, [_I32, _I32, _I32, _I32]),
     "mt_launch_count": (ctypes.c_longlong, []),
     "mt_prof_begin": (ctypes.c_int, [_I32]),
     "mt_prof_end": (ctypes.c_int, [_I32, _V, _V, _V, _V]),

@@ -36,7 +36,8 @@ int mt_logdet_impl(const Grid& g, double* out, double* work, cudaStream_t st);
 int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_t st);
 int mt_quad_impl(const Grid& g, const double* z, double* work, double* out, cudaStream_t st);
 int mt_matvec_lower_impl(const Grid& g, const double* v, double* out, cudaStream_t st);
-int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st);
+int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st, int which = 3);
+int mt_trinv_impl(const Grid& g, int k, cudaStream_t st);
 int mt_logdet_partials_impl(const Grid& g, double* partial, cudaStream_t st);
 int mt_sumsq_impl(const double* x, int64_t m, double* work, double* out, cudaStream_t st);
 int64_t mt_cross_work_doubles_impl(int64_t m, int64_t n);
@@ -70,15 +71,18 @@ static int check_layout(const mt_tiles* g) {
       g->t < 1 || g->t > g->p || g->mode < 0 || g->mode > 2 ||
       (g->mode == MT_MODE_DP && g->t != g->p) || !g->dp_pool || !g->status ||
       !g->scratch || (g->mode == MT_MODE_MP && g->t < g->p && !g->sp_pool) ||
-      g->col_stride < 0 || (g->col_stride > 1 && (g->col_offset < 0 ||
-                                                  g->col_offset >= g->col_stride || !g->dpanel))) {
+      g->col_stride < 0 || g->row_stride < 0 ||
+      ((g->col_stride > 1 || g->row_stride > 1) &&
+       (g->col_offset < 0 || g->col_offset >= (g->col_stride > 0 ? g->col_stride : 1) ||
+        g->row_offset < 0 || g->row_offset >= (g->row_stride > 0 ? g->row_stride : 1) ||
+        !g->dpanel))) {
     mt_set_error("bad tile layout descriptor");
     return MT_E_BAD_ARG;
   }
   return MT_OK;
 }
 static int single_gpu_only(const mt_tiles* g, const char* what) {
-  if (g->col_stride > 1) {
+  if (g->col_stride > 1 || g->row_stride > 1) {
     mt_set_error("%s operates on the full matrix; use the per-step multi-GPU entry points", what);
     return MT_E_BAD_ARG;
   }
@@ -412,17 +416,67 @@ int mt_cholesky(const mt_tiles* t, int32_t lookahead, void* stream) {
   return cholesky_schedule(make_grid(t), lookahead, (cudaStream_t)stream);
 }
 
-// ---- per-step entry points of the multi-GPU (tile-column-cyclic) factorization
-int mt_panel(const mt_tiles* t, int32_t k, void* stream) {
+// ---- per-step entry points of the multi-GPU (2D block-cyclic) factorization
+// POTRF(k) on the owner of tile (k, k); on a multi-GPU grid also the copy of
+// L_kk into the FP64 panel ring (row k) and W = L_kk^{-1} for the tensor-core
+// TRSM: what the column broadcast sends to the other ranks of process column k
+int mt_panel_factor(const mt_tiles* t, int32_t k, void* stream) {
   RC(check_layout(t));
   const Grid g = make_grid(t);
-  if (k < 0 || k >= g.p || !g.owns_col(k)) {
-    mt_set_error("mt_panel: rank does not own tile column %d", k);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k < 0 || k >= g.p || !g.owns(k, k)) {
+    mt_set_error("mt_panel_factor: rank does not own tile (%d, %d)", k, k);
     return MT_E_BAD_ARG;
   }
   const int narrow = (g.mode == MT_MODE_MP && k + g.t <= g.p - 1) ? 1 : 0;
-  RC(mt_potrf_impl(g, k, narrow, (cudaStream_t)stream));
+  RC(mt_potrf_impl(g, k, narrow, st));
+  if (g.multi() && g.dpanel)
+    CK(cudaMemcpyAsync(g.dpanel_tile(k, k), g.dtile(k, k), g.tile_elems() * sizeof(double),
+                       cudaMemcpyDeviceToDevice, st), "L_kk to panel ring");
+  if (g.multi() && g.mode == MT_MODE_MP && k + g.t < g.p && mt_tc_trsm_enabled(g))
+    RC(mt_trinv_impl(g, k, st));
+  return MT_OK;
+}
+
+// TRSM(k) of this rank's rows of tile column k (L_kk, its inverses and W present)
+int mt_panel_solve(const mt_tiles* t, int32_t k, void* stream) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  if (k < 0 || k >= g.p || !g.owns_col(k)) {
+    mt_set_error("mt_panel_solve: rank does not own tile column %d", k);
+    return MT_E_BAD_ARG;
+  }
   if (k + 1 < g.p) RC(mt_trsm_impl(g, k, (cudaStream_t)stream));
+  return MT_OK;
+}
+
+// both, on a rank that owns tile (k, k) and the whole of column k (1 x Q grids)
+int mt_panel(const mt_tiles* t, int32_t k, void* stream) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  if (k < 0 || k >= g.p || !g.owns_col(k) || g.rs > 1) {
+    mt_set_error("mt_panel: rank does not own tile column %d", k);
+    return MT_E_BAD_ARG;
+  }
+  RC(mt_panel_factor(t, k, stream));
+  return mt_panel_solve(t, k, stream);
+}
+
+// element ranges of what the column broadcast of panel k carries on a P x Q
+// grid (P > 1): {offset, count} of L_kk in dpanel (doubles), of the 32x32
+// diagonal-block inverses in scratch (floats), of W's split in split (floats)
+int mt_diag_regions(const mt_tiles* t, int32_t k, int64_t* out6) {
+  RC(check_layout(t));
+  const Grid g = make_grid(t);
+  if (!out6 || k < 0 || k >= g.p) { mt_set_error("mt_diag_regions: bad arguments"); return MT_E_BAD_ARG; }
+  const int64_t te = g.tile_elems();
+  out6[0] = g.dpanel ? (g.dpanel_tile(k, k) - g.dpanel) : 0;
+  out6[1] = g.dpanel ? te : 0;
+  out6[2] = (float*)g.sinv64(k) - g.scratch;
+  out6[3] = g.inv_tiles() * te;
+  const bool w = g.split && g.mode == MT_MODE_MP && k + g.t < g.p;
+  out6[4] = w ? g.winv_row() * g.nb : 0;
+  out6[5] = w ? 2 * te : 0;
   return MT_OK;
 }
 
@@ -469,7 +523,12 @@ int mt_logdet_partials(const mt_tiles* t, double* partial, void* stream) {
 
 int mt_fwd_step(const mt_tiles* t, int32_t i, double* x, void* stream) {
   RC(check_layout(t));
-  return mt_fwd_step_impl(make_grid(t), i, x, (cudaStream_t)stream);
+  return mt_fwd_step_impl(make_grid(t), i, x, (cudaStream_t)stream, 3);
+}
+
+int mt_fwd_step_ex(const mt_tiles* t, int32_t i, int32_t which, double* x, void* stream) {
+  RC(check_layout(t));
+  return mt_fwd_step_impl(make_grid(t), i, x, (cudaStream_t)stream, which);
 }
 
 int mt_sumsq(const double* x, int64_t m, double* work, double* out, void* stream) {
@@ -488,7 +547,46 @@ int mt_local_tiles(int32_t p, int32_t t_, int32_t mode, int32_t col_stride, int3
 }
 
 int64_t mt_dpanel_tiles(int32_t p, int32_t t_, int32_t mode) {
-  return 2 * (int64_t)(mode == MT_MODE_DP ? p : t_);
+  (void)t_; (void)mode;
+  return mt_dpanel_tiles_ex(p, 1, 2);
+}
+
+int mt_local_tiles_ex(int32_t p, int32_t t_, int32_t mode, int32_t row_stride, int32_t row_offset,
+                      int32_t col_stride, int32_t col_offset, int64_t* ndp, int64_t* nsp) {
+  Grid g{};
+  g.p = p; g.t = mode == MT_MODE_DP ? p : t_; g.mode = mode;
+  g.cs = col_stride > 0 ? col_stride : 1; g.c0 = col_offset;
+  g.rs = row_stride > 0 ? row_stride : 1; g.r0 = row_offset;
+  if (ndp) *ndp = g.nband();
+  if (nsp) *nsp = g.noff();
+  return MT_OK;
+}
+
+// both panel rings hold every tile row (ring order): 2 panels x pring tiles
+int64_t mt_dpanel_tiles_ex(int32_t p, int32_t row_stride, int32_t col_stride) {
+  Grid g{};
+  g.p = p;
+  g.rs = row_stride > 0 ? row_stride : 1;
+  g.cs = col_stride > 0 ? col_stride : 1;
+  return 2 * (int64_t)g.pring();
+}
+
+int64_t mt_split_tiles_ex(int32_t p, int32_t t_, int32_t mode, int32_t row_stride,
+                          int32_t col_stride) {
+  if (!(mode == MT_MODE_MP && t_ < p)) return 0;
+  Grid g{};
+  g.p = p;
+  g.rs = row_stride > 0 ? row_stride : 1;
+  g.cs = col_stride > 0 ? col_stride : 1;
+  return 4 * (int64_t)g.pring() + 2 * (int64_t)p + 2;
+}
+
+int32_t mt_ring_pos(int32_t p, int32_t row_stride, int32_t col_stride, int32_t i) {
+  Grid g{};
+  g.p = p;
+  g.rs = row_stride > 0 ? row_stride : 1;
+  g.cs = col_stride > 0 ? col_stride : 1;
+  return g.ring_pos(i);
 }
 
 int64_t mt_work_doubles(const mt_tiles* t) {
@@ -568,7 +666,7 @@ static int tile_xfer(const mt_tiles* t, int32_t i, int32_t j, int32_t which, voi
   RC(check_layout(t));
   const Grid g = make_grid(t);
   if (i < 0 || j < 0 || i >= g.p || j > i || !g.present(i, j) || (which == 0) != g.band(i, j) ||
-      !g.owns_col(j)) {
+      !g.owns(i, j)) {
     mt_set_error("tile (%d,%d) not stored in the requested pool", i, j);
     return MT_E_BAD_ARG;
   }

@@ -85,21 +85,21 @@ __device__ __forceinline__ Src operand(const Grid& g, const Maps& maps, int i, i
   s.lo = 0;
   if (g.band(i, k)) {
     s.kind = KF64;
-    if (g.cs == 1) {
+    if (!g.multi()) {
       s.map = &maps.dp;
-      s.row = (int)((g.bcol(k) + (i - k)) * g.nb) + r0;
+      s.row = (int)(g.dslot(i, k) * g.nb) + r0;
     } else {
       s.map = &maps.dpanel;
-      s.row = (int)(((int64_t)(k & 1) * g.t + (i - k)) * g.nb) + r0;
+      s.row = (int)g.dpanel_row(i, k) + r0;
     }
-  } else if (g.cs == 1) {
+  } else if (!g.multi()) {
     s.kind = KF32;
     s.map = &maps.sp;
-    s.row = (int)((g.scol(k) + (i - k - g.t)) * g.nb) + r0;
+    s.row = (int)(g.sslot(i, k) * g.nb) + r0;
   } else {
     s.kind = KSPLIT;
     s.map = &maps.split;
-    s.row = (int)(((int64_t)(k & 1) * g.p + i) * 2 * g.nb) + r0;
+    s.row = (int)g.split_row(i, k) + r0;
     s.lo = g.nb;
   }
   return s;
@@ -268,10 +268,10 @@ int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStre
   const int64_t sp_rows = g.sp ? g.noff() * nb : nb;
   if (!rc) rc = make_map_2d(&maps.sp, sp, sp_rows, nb, 4, BK, 64, CU_TENSOR_MAP_SWIZZLE_64B);
   const void* spl = g.split ? (const void*)g.split : (const void*)g.dp;
-  const int64_t spl_rows = g.split ? (int64_t)4 * g.p * nb : nb;
+  const int64_t spl_rows = g.split ? (int64_t)4 * g.pring() * nb : nb;
   if (!rc) rc = make_map_2d(&maps.split, spl, spl_rows, nb, 4, BK, 64, CU_TENSOR_MAP_SWIZZLE_64B);
   const void* dpn = g.dpanel ? (const void*)g.dpanel : (const void*)g.dp;
-  const int64_t dpn_rows = g.dpanel ? (int64_t)2 * g.t * nb : nb;
+  const int64_t dpn_rows = g.dpanel ? (int64_t)2 * g.pring() * nb : nb;
   if (!rc) rc = make_map_2d(&maps.dpanel, dpn, dpn_rows, nb, 8, BK, 64, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   const int nsm = nb / BM, nsn = nb / BN;

@@ -16,6 +16,22 @@
 
 #define MT_HD __host__ __device__ __forceinline__
 
+// sum_{x=0}^{n-1} floor((a x + b) / m), a, b >= 0, m > 0 (Euclid-like, O(log))
+MT_HD int64_t mt_floor_sum(int64_t n, int64_t m, int64_t a, int64_t b) {
+  int64_t ans = 0;
+  while (n > 0) {
+    if (a >= m) { ans += (n - 1) * n / 2 * (a / m); a %= m; }
+    if (b >= m) { ans += n * (b / m); b %= m; }
+    const int64_t y = a * n + b;
+    if (y < m) break;
+    n = y / m;
+    b = y % m;
+    const int64_t tmp = m; m = a; a = tmp;
+  }
+  return ans;
+}
+MT_HD int mt_gcd(int a, int b) { while (b) { const int r = a % b; a = b; b = r; } return a; }
+
 struct Grid {
   int64_t n;
   int nb, p, t, mode;
@@ -24,10 +40,12 @@ struct Grid {
   float* scratch;
   int64_t* status;
   float* split;
-  // multi-GPU tile-column-cyclic ownership: this rank stores tile columns
-  // j = c0, c0 + cs, c0 + 2cs, ... (single GPU: cs = 1, c0 = 0)
+  // multi-GPU 2D block-cyclic ownership on a P x Q process grid: this rank
+  // stores tiles (i, j) with i = r0 (mod rs) and j = c0 (mod cs), rs = P,
+  // cs = Q (single GPU: rs = cs = 1, r0 = c0 = 0)
   int cs = 1, c0 = 0;
-  double* dpanel = nullptr;  // multi-GPU: FP64 band rows of the panels in flight
+  int rs = 1, r0 = 0;
+  double* dpanel = nullptr;  // multi-GPU: FP64 rows of the two panels in flight (ring)
   // bulk FP32 update only: SM-yield request word written by the panel stream
   // (cuStreamWriteValue32); CTAs that consume a request exit between work items
   int* yield = nullptr;
@@ -35,42 +53,82 @@ struct Grid {
   MT_HD int64_t tile_elems() const { return (int64_t)nb * nb; }
   MT_HD bool band(int i, int j) const { return (i - j) < t; }
   MT_HD bool present(int i, int j) const { return mode != MT_MODE_DST || (i - j) < t; }
+  MT_HD bool multi() const { return cs > 1 || rs > 1; }
   // logical rows of tile row i (ragged edge, tilestore.py:154-156)
   MT_HD int rows(int i) const {
     int64_t r = n - (int64_t)i * nb;
     return r < nb ? (int)r : nb;
   }
   MT_HD bool owns_col(int j) const { return j >= c0 && (j - c0) % cs == 0; }
+  MT_HD bool owns_row(int i) const { return i >= r0 && (i - r0) % rs == 0; }
+  MT_HD bool owns(int i, int j) const { return owns_row(i) && owns_col(j); }
   // number of owned tile columns j' < j
   MT_HD int owned_before(int j) const { return j <= c0 ? 0 : (j - c0 + cs - 1) / cs; }
   MT_HD int owned_cols() const { return owned_before(p); }
   MT_HD int owned_col(int m) const { return c0 + m * cs; }
+  // owned tile rows i' < x (x >= 0), and the first owned row >= x
+  MT_HD int rcnt(int x) const { return rs == 1 ? x : (x - r0 + rs - 1) / rs; }
+  MT_HD int first_row(int x) const { return rs == 1 ? x : x + ((r0 - x) % rs + rs) % rs; }
+  // sum over owned columns m < mm of rcnt(j_m + d)  (j_m = c0 + m cs)
+  MT_HD int64_t rcnt_sum(int mm, int d) const {
+    return mt_floor_sum(mm, rs, cs, (int64_t)c0 + d - r0 + rs - 1);
+  }
 
-  // first band-pool slot of tile column j: sum over owned j' < j of min(t, p - j')
+  // first band-pool slot of tile column j: sum over owned j' < j of the owned
+  // rows in [j', min(j' + t, p))
   MT_HD int64_t bcol(int j) const {
     const int m = owned_before(j);
-    const int m1 = owned_before(p - t + 1);  // owned columns holding t band tiles
-    if (m <= m1) return (int64_t)m * t;
-    return (int64_t)m1 * t + (int64_t)(m - m1) * (p - c0) -
-           (int64_t)cs * ((int64_t)m * (m - 1) / 2 - (int64_t)m1 * (m1 - 1) / 2);
+    const int m1 = owned_before(p - t + 1);  // owned columns holding t band rows
+    if (rs == 1) {
+      if (m <= m1) return (int64_t)m * t;
+      return (int64_t)m1 * t + (int64_t)(m - m1) * (p - c0) -
+             (int64_t)cs * ((int64_t)m * (m - 1) / 2 - (int64_t)m1 * (m1 - 1) / 2);
+    }
+    const int ma = m < m1 ? m : m1;
+    int64_t s = rcnt_sum(ma, t) - rcnt_sum(ma, 0);
+    if (m > m1) s += (int64_t)(m - m1) * rcnt(p) - (rcnt_sum(m, 0) - rcnt_sum(m1, 0));
+    return s;
   }
-  // first off-band-pool slot of tile column j: sum over owned j' < j of max(0, p - t - j')
+  // first off-band-pool slot of tile column j: sum over owned j' < j of the
+  // owned rows in [j' + t, p)
   MT_HD int64_t scol(int j) const {
     const int64_t q = p - t;
     if (q <= 0) return 0;
     const int ma = owned_before(j), mb = owned_before((int)q);
     const int mm = ma < mb ? ma : mb;
-    return (int64_t)mm * (q - c0) - (int64_t)cs * ((int64_t)mm * (mm - 1) / 2);
+    if (rs == 1) return (int64_t)mm * (q - c0) - (int64_t)cs * ((int64_t)mm * (mm - 1) / 2);
+    return (int64_t)mm * rcnt(p) - rcnt_sum(mm, t);
   }
   MT_HD int64_t nband() const { return bcol(p); }
   MT_HD int64_t noff() const { return mode == MT_MODE_MP ? scol(p) : 0; }
-  // multi-GPU panel ring: FP64 copy of band rows i in [k, k + t) of panel k
-  MT_HD double* dpanel_tile(int i, int k) const {
-    return dpanel + ((int64_t)(k & 1) * t + (i - k)) * tile_elems();
-  }
+  // pool slot of an owned tile
+  MT_HD int64_t dslot(int i, int j) const { return bcol(j) + (rcnt(i) - rcnt(j)); }
+  MT_HD int64_t sslot(int i, int j) const { return scol(j) + (rcnt(i) - rcnt(j + t)); }
 
-  MT_HD double* dtile(int i, int j) const { return dp + (bcol(j) + (i - j)) * tile_elems(); }
-  MT_HD float* stile(int i, int j) const { return sp + (scol(j) + (i - j - t)) * tile_elems(); }
+  // panel ring order (multi-GPU): tile rows grouped by i mod L, L = lcm(P, Q)
+  // (1 on a 1 x Q grid), so the rows a process row or column receives are
+  // contiguous suffixes of L blocks; single GPU: identity
+  MT_HD int ring_l() const { return rs == 1 ? 1 : rs / mt_gcd(rs, cs) * cs; }
+  MT_HD int ring_q() const { return (p + ring_l() - 1) / ring_l(); }
+  MT_HD int pring() const { return ring_l() * ring_q(); }
+  MT_HD int ring_pos(int i) const {
+    const int l = ring_l();
+    return l == 1 ? i : (i % l) * ring_q() + i / l;
+  }
+  // multi-GPU panel ring: FP64 rows of panel k (band rows in MP; all in DP)
+  MT_HD double* dpanel_tile(int i, int k) const {
+    return dpanel + ((int64_t)(k & 1) * pring() + ring_pos(i)) * tile_elems();
+  }
+  MT_HD int64_t dpanel_row(int i, int k) const {
+    return ((int64_t)(k & 1) * pring() + ring_pos(i)) * nb;
+  }
+  // L_kk for the panel solves: the pool tile on its owner, else the copy
+  // broadcast into the FP64 panel ring (row k of panel k)
+  MT_HD const double* diag_tile(int k) const {
+    return (!multi() || owns(k, k)) ? dtile(k, k) : dpanel_tile(k, k);
+  }
+  MT_HD double* dtile(int i, int j) const { return dp + dslot(i, j) * tile_elems(); }
+  MT_HD float* stile(int i, int j) const { return sp + sslot(i, j) * tile_elems(); }
 
   // scratch ring: slot s holds [narrowed L_kk][mirrors of band panel rows k+1..k+t-1]
   // (MP, t < p) followed by one tile holding the inverses of L_kk's 32x32 diagonal
@@ -89,16 +147,19 @@ struct Grid {
     return (double*)(sslot(k) + (has_mirrors() ? (int64_t)t : 0) * tile_elems());
   }
   MT_HD float* sinv32(int k) const { return (float*)(sinv64(k) + (int64_t)nblk32() * 1024); }
-  // TF32 hi/lo split of FP32 operand (i, k) of panel k (tensor-core engine)
-  MT_HD float* split_hi(int i, int k) const {
-    return split + ((int64_t)(k & 1) * p + i) * 2 * tile_elems();
+  // TF32 hi/lo split of FP32 operand (i, k) of panel k (tensor-core engine),
+  // ring of two panels in ring order: rows of [hi | lo] per tile row
+  MT_HD int64_t split_row(int i, int k) const {
+    return ((int64_t)(k & 1) * pring() + ring_pos(i)) * 2 * nb;
   }
+  MT_HD float* split_hi(int i, int k) const { return split + split_row(i, k) * nb; }
   MT_HD float* split_lo(int i, int k) const { return split_hi(i, k) + tile_elems(); }
   // split buffer tail (tensor-core TRSM): the pre-TRSM split of the next
   // panel's off-band tiles (written by the update epilogue into column k+1)
   // and the split of W = L_kk^{-1} (row-major), one slot each
-  MT_HD int64_t presplit_row(int i) const { return ((int64_t)4 * p + 2 * i) * nb; }
-  MT_HD int64_t winv_row() const { return (int64_t)6 * p * nb; }
+  MT_HD int64_t presplit_row(int i) const { return ((int64_t)4 * pring() + 2 * i) * nb; }
+  MT_HD int64_t winv_row() const { return ((int64_t)4 * pring() + 2 * p) * nb; }
+  MT_HD int64_t split_rows() const { return ((int64_t)4 * pring() + 2 * p + 2) * nb; }
   MT_HD float* presplit_hi(int i) const { return split + presplit_row(i) * nb; }
   MT_HD float* winv_hi() const { return split + winv_row() * nb; }
   MT_HD float* winv_lo() const { return winv_hi() + tile_elems(); }
@@ -109,6 +170,8 @@ struct Grid {
   }
 
   // slot -> (i, j) inversion by binary search over the owned column starts
+  // (a column without owned rows shares its start with the next column, so
+  // the largest index with start <= s is a column that holds slot s)
   __device__ __forceinline__ void band_slot_ij(int64_t s, int& i, int& j) const {
     int lo = 0, hi = owned_cols();  // largest owned index m with bcol(col m) <= s
     while (hi - lo > 1) {
@@ -116,7 +179,7 @@ struct Grid {
       if (bcol(owned_col(mid)) <= s) lo = mid; else hi = mid;
     }
     j = owned_col(lo);
-    i = j + (int)(s - bcol(j));
+    i = first_row(j) + (int)(s - bcol(j)) * rs;
   }
   __device__ __forceinline__ void off_slot_ij(int64_t s, int& i, int& j) const {
     int lo = 0, hi = owned_before(p - t);
@@ -125,7 +188,7 @@ struct Grid {
       if (scol(owned_col(mid)) <= s) lo = mid; else hi = mid;
     }
     j = owned_col(lo);
-    i = j + t + (int)(s - scol(j));
+    i = first_row(j + t) + (int)(s - scol(j)) * rs;
   }
   __device__ __forceinline__ bool failed() const {
     return *(volatile int64_t*)status >= 0;
@@ -189,6 +252,8 @@ inline Grid make_grid(const mt_tiles* g) {
   r.split = g->split;
   r.cs = g->col_stride > 0 ? g->col_stride : 1;
   r.c0 = g->col_offset;
+  r.rs = g->row_stride > 0 ? g->row_stride : 1;
+  r.r0 = g->row_offset;
   r.dpanel = g->dpanel;
   return r;
 }
@@ -289,7 +354,7 @@ bool mt_tc2w_supported(const Grid& g);
 int mt_tc2w_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cudaStream_t st,
                    unsigned long long* span);
 int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm, int presplit,
-                  cudaStream_t st, unsigned long long* span);
+                  cudaStream_t st, unsigned long long* span, int jlo = 0, int jhi = 0);
 int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm,
                   int presplit, cudaStream_t st, unsigned long long* span = nullptr, int jlo = 0,
                   int jhi = 0);

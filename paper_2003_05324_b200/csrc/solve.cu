@@ -38,7 +38,7 @@ __device__ __forceinline__ bool tile_ref(const Grid& g, int i, int j, TileRef& t
 // ------------------------------------------------------------------ logdet
 __global__ void __launch_bounds__(256) logdet_partial_kernel(Grid g, double* partial) {
   const int k = blockIdx.x;
-  if (!g.owns_col(k)) {  // multi-GPU: another rank holds this diagonal tile
+  if (!g.owns(k, k)) {  // multi-GPU: another rank holds this diagonal tile
     if (threadIdx.x == 0) partial[k] = 0.0;
     return;
   }
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) gemv_fwd_kernel(Grid g, int i, double* x,
   const int r_tile = i + 1 + blockIdx.x / nrb;
   const int rb = blockIdx.x % nrb;
   TileRef T;
-  if (!tile_ref(g, r_tile, i, T)) return;
+  if (!g.owns_row(r_tile) || !tile_ref(g, r_tile, i, T)) return;
   const int nb = g.nb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* yi = x + (int64_t)i * nb * nrhs;
@@ -312,18 +312,24 @@ int mt_solve_impl(const Grid& g, double* x, int64_t nrhs, int which, cudaStream_
   return MT_OK;
 }
 
-// multi-GPU forward sweep, step i (on the owner of tile column i): y_i = L_ii^{-1} x_i,
-// then x_r -= L_ri y_i for r > i -- the same launches and order as mt_solve_impl
-int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st) {
+// multi-GPU forward sweep, step i: on the owner of tile (i, i) y_i = L_ii^{-1} x_i
+// (which = 1), on the ranks of tile column i x_r -= L_ri y_i for their rows r > i
+// (which = 2) -- the same kernels and order as mt_solve_impl
+int mt_fwd_step_impl(const Grid& g, int i, double* x, cudaStream_t st, int which) {
   const int nb = g.nb, p = g.p;
-  if (!g.owns_col(i)) { mt_set_error("rank does not own tile column %d", i); return MT_E_BAD_ARG; }
+  if (((which & 1) && !g.owns(i, i)) || ((which & 2) && !g.owns_col(i))) {
+    mt_set_error("rank does not own the tiles of forward-sweep step %d", i);
+    return MT_E_BAD_ARG;
+  }
   const size_t smem = (size_t)nb * sizeof(double);
   cudaFuncSetAttribute(trsv_fwd_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(smem > 48 * 1024 ? smem : 48 * 1024));
   ProfScope ps(MT_K_SOLVE, st, 2.0 * (double)nb * nb * (p - i), (double)nb * nb * 8.0 * (p - i), 2);
-  trsv_fwd_diag_kernel<<<1, 512, smem, st>>>(g, i, x, 1);
-  MT_LAUNCH_CHECK("trsv_fwd_diag");
-  if (i + 1 < p) {
+  if (which & 1) {
+    trsv_fwd_diag_kernel<<<1, 512, smem, st>>>(g, i, x, 1);
+    MT_LAUNCH_CHECK("trsv_fwd_diag");
+  }
+  if ((which & 2) && i + 1 < p) {
     const int nrb = (nb + kGemvRows - 1) / kGemvRows;
     gemv_fwd_kernel<<<(unsigned)((p - i - 1) * nrb), 256, 0, st>>>(g, i, x, 1, nrb);
     MT_LAUNCH_CHECK("gemv_fwd");

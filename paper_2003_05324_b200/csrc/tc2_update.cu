@@ -244,8 +244,8 @@ __device__ __forceinline__ void tc2_body(const Grid& g, int k, const Work2& w,
         const int n0 = (sub % w.nsubn) * BN + (int)rank * BNH;
         // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb;
         // TRSM: A = pre-split of B_ik, B = split of W = L_kk^{-1}
-        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
-        const int brow = TRSM ? (int)g.winv_row() + n0 : ((k & 1) * g.p + j) * 2 * nb + n0;
+        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : (int)g.split_row(i, k) + m0;
+        const int brow = TRSM ? (int)g.winv_row() + n0 : (int)g.split_row(j, k) + n0;
         const int ksteps = item_ksteps(item);
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int st = it % STAGES;
@@ -500,7 +500,7 @@ int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
                   int presplit, cudaStream_t st, unsigned long long* span, int jlo, int jhi) {
   if (scnt <= 0) return MT_OK;
   CUtensorMap ma, mb;
-  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
+  const int64_t split_rows = g.split_rows();
   int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
   // C (off-band pool) in 32 x 32 FP32 chunks for the TMA epilogue
@@ -518,7 +518,7 @@ int mt_tc2_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   w.span = span;
   w.mlo = g.owned_before(jlo);
   w.mhi = g.owned_before(jhi);
-  w.sw = (!trsm && jhi > jlo + 1) ? mt_opt_super_cols() : 0;
+  w.sw = (!trsm && jhi > jlo + 1 && g.rs == 1) ? mt_opt_super_cols() : 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_sm2) cudaDeviceGetAttribute(&g_sm2, cudaDevAttrMultiProcessorCount, dev);

@@ -177,8 +177,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         if (item < 0) break;
         const int m0 = (item % w.nsubm) * (2 * BM) + (int)rank * BM;
-        const int arow = ((k & 1) * g.p + i) * 2 * nb + m0;
-        const int brow = ((k & 1) * g.p + j) * 2 * nb + (int)rank * BNH;  // + h * 256
+        const int arow = (int)g.split_row(i, k) + m0;
+        const int brow = (int)g.split_row(j, k) + (int)rank * BNH;  // + h * 256
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int st = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -344,7 +344,7 @@ int mt_tc2w_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, cud
                    unsigned long long* span) {
   if (scnt <= 0) return MT_OK;
   CUtensorMap ma, mb, mc;
-  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
+  const int64_t split_rows = g.split_rows();
   int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
   const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;

@@ -198,8 +198,8 @@ __device__ __forceinline__ void tc32_body(const Grid& g, int k, const Work& w,
         }
         // split buffer rows: hi of tile (i, k) at ((k&1)*p + i)*2*nb, lo at + nb;
         // TRSM: A = pre-split of B_ik, B = split of W = L_kk^{-1}
-        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
-        const int brow = TRSM ? (int)g.winv_row() + n0 : ((k & 1) * g.p + j) * 2 * nb + n0;
+        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : (int)g.split_row(i, k) + m0;
+        const int brow = TRSM ? (int)g.winv_row() + n0 : (int)g.split_row(j, k) + n0;
         const int ksteps = item_ksteps(item);
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int s = it % STAGES;
@@ -421,11 +421,11 @@ int make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, in
 
 bool mt_tc_supported(const Grid& g) {
   return g.mode == MT_MODE_MP && g.split != nullptr && g.nb % BN == 0 &&
-         ((int64_t)6 * g.p + 2) * g.nb < (1ll << 31);
+         g.split_rows() < (1ll << 31);
 }
 
 bool mt_tc_trsm_enabled(const Grid& g) {
-  return mt_opt_tc_trsm() && (mt_engine_tc(mt_opt_engine()) || g.cs > 1) &&
+  return mt_opt_tc_trsm() && (mt_engine_tc(mt_opt_engine()) || g.multi()) &&
          mt_tc_supported(g);
 }
 
@@ -438,7 +438,7 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
   // kernels below accumulate the whole K range in TMEM (opt-in engine 2)
   if (mt_opt_engine() != MT_ENGINE_TF32X3_RZ)
     return mt_tcf_launch(g, k, s0, scnt, ctas, trsm, (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st,
-                         span);
+                         span, jlo, jhi);
   // full-width (256 x 512) CTA-pair items for the bulk update (tc2w_update.cu)
   if (!trsm && mt_opt_wide_items() && mt_opt_cta_pairs() && mt_tc2w_supported(g) && jlo > k + 1 &&
       !mt_opt_tc_diag() && !mt_opt_c_prefetch() && mt_opt_super_cols() == 0)
@@ -447,7 +447,7 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
     return mt_tc2_launch(g, k, s0, scnt, ctas, trsm,
                          (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0, st, span, jlo, jhi);
   CUtensorMap ma, mb;
-  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;  // whole split buffer
+  const int64_t split_rows = g.split_rows();  // whole split buffer
   int rc = make_map(&ma, g.split, split_rows, g.nb, BM);
   if (!rc) rc = make_map(&mb, g.split, split_rows, g.nb, BN);
   if (rc) return rc;
@@ -459,7 +459,7 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
   w.presplit = (!trsm && mt_tc_trsm_enabled(g)) ? 1 : 0;
   w.mlo = g.owned_before(jlo);
   w.mhi = g.owned_before(jhi);
-  w.sw = (!trsm && jhi > jlo) ? mt_opt_super_cols() : 0;
+  w.sw = (!trsm && jhi > jlo && g.rs == 1) ? mt_opt_super_cols() : 0;
   w.l2pf = trsm ? 0 : mt_opt_c_prefetch();
   w.diag = trsm ? 0 : mt_opt_tc_diag();
   int dev = 0;

@@ -112,6 +112,7 @@ struct WorkF {
   int* counter;  // [work queue head, pairs started]
   int presplit;  // the column-(k+1) update also writes its outputs' TF32 split
   unsigned long long* span;
+  int mlo, mhi, sw;  // update: owned column range, super-column width (0 = slot order)
 };
 
 enum { OUT_UPDATE = 0, OUT_PRESPLIT = 1, OUT_TRSM = 2 };
@@ -212,7 +213,10 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
             item = atomicAdd(w.counter, 1);
             if (item >= w.nitems) item = -1;
           }
-          if (item >= 0) g.off_slot_ij(w.slot0 + item / nsub, i, j);
+          if (item >= 0) {
+            if (!TRSM && w.sw > 0) super_tile_ij(g, item / nsub, w.mlo, w.mhi, w.sw, i, j);
+            else g.off_slot_ij(w.slot0 + item / nsub, i, j);
+          }
           sitem[s] = item; si[s] = i; sj[s] = j;
           st_cl_u32(peer_addr(&sitem[s], 1), (uint32_t)item);
           st_cl_u32(peer_addr(&si[s], 1), (uint32_t)i);
@@ -230,8 +234,8 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
         const int sub = item % nsub;
         const int m0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM;
         const int n0 = (sub % w.nsubn) * BN + (int)rank * BNH;
-        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : ((k & 1) * g.p + i) * 2 * nb + m0;
-        const int brow = TRSM ? (int)g.winv_row() + n0 : ((k & 1) * g.p + j) * 2 * nb + n0;
+        const int arow = TRSM ? (int)g.presplit_row(i) + m0 : (int)g.split_row(i, k) + m0;
+        const int brow = TRSM ? (int)g.winv_row() + n0 : (int)g.split_row(j, k) + n0;
         const int ksteps = item_ksteps(item);
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int st = it % STAGES;
@@ -315,8 +319,8 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
       const int out = TRSM ? OUT_TRSM : ((w.presplit && j == k + 1) ? OUT_PRESPLIT : OUT_UPDATE);
       // TMA rows: output tile (i, j) (TRSM: j == k) in the off-band pool, and
       // the split buffer rows of its TF32 hi part (lo = + nb)
-      const int crow = (int)((g.scol(j) + (i - j - g.t)) * (int64_t)nb) + row0;
-      const int srow = out == OUT_TRSM ? (int)(((int64_t)(k & 1) * g.p + i) * 2 * nb) + row0
+      const int crow = (int)(g.sslot(i, j) * nb) + row0;
+      const int srow = out == OUT_TRSM ? (int)g.split_row(i, k) + row0
                                        : (int)g.presplit_row(i) + row0;
       const int nch = item_ksteps(item) / KC;
       float sum[COLS_W];
@@ -471,10 +475,10 @@ int g_smf = 0;
 // launch over the off-band slot range [s0, s0 + scnt) of step k (update) or
 // panel k (trsm); `ctas` caps the grid (rounded down to pairs)
 int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm, int presplit,
-                  cudaStream_t st, unsigned long long* span) {
+                  cudaStream_t st, unsigned long long* span, int jlo, int jhi) {
   if (scnt <= 0) return MT_OK;
   CUtensorMap ma, mb, mc, ms;
-  const int64_t split_rows = ((int64_t)6 * g.p + 2) * g.nb;
+  const int64_t split_rows = g.split_rows();
   int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
   const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;
@@ -489,6 +493,9 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   w.nitems = (int)(scnt * w.nsubm * w.nsubn);
   w.presplit = presplit;
   w.span = span;
+  w.mlo = g.owned_before(jlo);
+  w.mhi = g.owned_before(jhi);
+  w.sw = (!trsm && jhi > jlo + 1 && g.rs == 1) ? mt_opt_super_cols() : 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_smf) cudaDeviceGetAttribute(&g_smf, cudaDevAttrMultiProcessorCount, dev);

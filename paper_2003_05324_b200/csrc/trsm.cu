@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* M = nullptr;
   if constexpr (sizeof(T) == 8) {
     g.band_slot_ij(slot, i, j);
-    L = (const T*)g.dtile(k, k);
+    L = (const T*)g.diag_tile(k);
     Linv = (const T*)g.sinv64(k);
     B = (T*)g.dtile(i, k);
     if (mirror_ok && g.mode == MT_MODE_MP && i + g.t <= g.p - 1) M = g.smirror(i, k);
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool fp32_operand = (sizeof(T) == 4) || (M != nullptr);
   float* SH = (g.split && fp32_operand) ? g.split_hi(i, k) : nullptr;
   float* SL = SH ? g.split_lo(i, k) : nullptr;
-  double* DP = (sizeof(T) == 8 && g.cs > 1 && g.dpanel) ? g.dpanel_tile(i, k) : nullptr;
+  double* DP = (sizeof(T) == 8 && g.multi() && g.dpanel) ? g.dpanel_tile(i, k) : nullptr;
   for (int r = threadIdx.x >> 5; r < nr; r += kThreads / 32) {
     for (int cc = c; cc < nb; cc += 32) {
       const T v = Xt[(size_t)cc * XS + r];
@@ -391,8 +391,11 @@ int mt_presplit_impl(const Grid& g, int k, cudaStream_t st) {
   return MT_OK;
 }
 
-// Panel rows i in (k, p) of tile column k.  Band rows: band slots
-// bcol(k)+1 .. bcol(k+1)-1; off-band rows: off slots scol(k) .. scol(k+1)-1.
+// Panel rows i in (k, p) of tile column k that this rank stores.  Band rows:
+// the band slots of column k after the diagonal tile (when it is ours);
+// off-band rows: off slots scol(k) .. scol(k+1)-1.  On a multi-GPU grid
+// W = L_kk^{-1} is formed by the diagonal tile's owner (mt_panel_factor) and
+// broadcast down the process column with L_kk and its 32x32 inverses.
 int mt_trsm_impl(const Grid& g, int k, cudaStream_t st, const std::function<int()>* before) {
   auto pre = [&]() { return before ? (*before)() : MT_OK; };
   if (trsm_smem<double, 32>(g.nb) > 220 * 1024 || trsm_smem<float, 64>(g.nb) > 220 * 1024) {
@@ -400,14 +403,17 @@ int mt_trsm_impl(const Grid& g, int k, cudaStream_t st, const std::function<int(
     return MT_E_BAD_ARG;
   }
   RC_(pre());
-  int rc = launch_trsm<double, 32>(g, k, g.bcol(k) + 1, g.bcol(k + 1) - g.bcol(k) - 1, 1, st);
+  const int64_t b0 = g.bcol(k) + (g.owns(k, k) ? 1 : 0);
+  int rc = launch_trsm<double, 32>(g, k, b0, g.bcol(k + 1) - b0, 1, st);
   if (rc) return rc;
   if (g.mode == MT_MODE_MP && g.scol(k + 1) > g.scol(k)) {
     if (mt_tc_trsm_enabled(g)) {
       // the update epilogue of step k-1 pre-split column k (k = 0: nobody did)
       if (k == 0) RC_(mt_presplit_impl(g, k, st));
-      RC_(pre());
-      RC_(mt_trinv_impl(g, k, st));
+      if (!g.multi()) {
+        RC_(pre());
+        RC_(mt_trinv_impl(g, k, st));
+      }
       RC_(pre());
       rc = mt_tc_trsm_impl(g, k, st);
     } else {

@@ -203,9 +203,9 @@ __device__ __forceinline__ Operand panel_operand(const Grid& g, int i, int k) {
   Operand o;
   o.lo = nullptr;
   if (g.band(i, k)) {
-    o.base = g.cs == 1 ? (const void*)g.dtile(i, k) : (const void*)g.dpanel_tile(i, k);
+    o.base = !g.multi() ? (const void*)g.dtile(i, k) : (const void*)g.dpanel_tile(i, k);
     o.f32 = false;
-  } else if (g.cs == 1) {
+  } else if (!g.multi()) {
     o.base = g.stile(i, k);
     o.f32 = true;
   } else {
@@ -374,17 +374,20 @@ static void update_flops(const Grid& g, int k, int jlo, int jhi, double& f64, do
   f64 = f32 = 0.0;
   const double rk = g.rows(k);
   for (int j = jlo; j < jhi; ++j) {
-    if (!g.owns_col(j)) continue;
+    if (!g.owns_col(j)) continue;  // (rows: only this rank's, below)
     const double rj = g.rows(j);
     const int iband = j + g.t < g.p ? j + g.t : g.p;  // band rows [j, iband)
     for (int i = j; i < iband; ++i) {
-      if (!g.present(i, k)) continue;
+      if (!g.present(i, k) || !g.owns_row(i)) continue;
       const double ri = g.rows(i);
       f64 += (i == j) ? ri * ri * rk : 2.0 * ri * rj * rk;
     }
     if (g.mode == MT_MODE_MP && iband < g.p) {  // off-band rows [iband, p): last may be ragged
-      const double cnt = g.p - iband;
-      f32 += 2.0 * rj * rk * ((cnt - 1) * g.nb + g.rows(g.p - 1));
+      const double cnt = g.rcnt(g.p) - g.rcnt(iband);
+      if (cnt > 0) {
+        const double last = g.owns_row(g.p - 1) ? g.rows(g.p - 1) : g.nb;
+        f32 += 2.0 * rj * rk * ((cnt - 1) * g.nb + last);
+      }
     }
   }
 }
@@ -395,7 +398,7 @@ static void update_flops(const Grid& g, int k, int jlo, int jhi, double& f64, do
 int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   if (jlo >= jhi) return MT_OK;
   const int nb = g.nb;
-  if (g.cs > 1 && (nb % MBM != 0 || (g.mode == MT_MODE_MP && !mt_tc_supported(g)))) {
+  if (g.multi() && (nb % MBM != 0 || (g.mode == MT_MODE_MP && !mt_tc_supported(g)))) {
     mt_set_error("multi-GPU layout needs nb %% 256 == 0 and the tcgen05 engine (split buffer)");
     return MT_E_BAD_ARG;
   }
@@ -412,7 +415,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t co_s0 = g.scol(jlo), co_scnt = g.scol(jhi) - co_s0;
   const int64_t co_b0 = g.bcol(jlo), co_bcnt = g.bcol(jhi) - co_b0;
   if (mt_opt_coschedule() && !pcol && g.mode == MT_MODE_MP && co_scnt > 0 && co_bcnt > 0 &&
-      (mt_engine_tc(mt_opt_engine()) || g.cs > 1) && mt_tc_supported(g) &&
+      (mt_engine_tc(mt_opt_engine()) || g.multi()) && mt_tc_supported(g) &&
       mt_opt_cta_pairs() && mt_opt_legacy_dmma() != 1 && mt_dmma_tma_supported(g)) {
     static int sms = 0;
     if (!sms) {
@@ -460,7 +463,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t s0 = g.scol(jlo), scnt = g.scol(jhi) - s0;
   if (scnt > 0) {
     ProfScope ps(pcol ? MT_K_UPD32P : MT_K_UPD32, st, f32, scnt * (double)nb * nb * 4.0 * 2.0);
-    if ((mt_engine_tc(mt_opt_engine()) || g.cs > 1) && mt_tc_supported(g)) {
+    if ((mt_engine_tc(mt_opt_engine()) || g.multi()) && mt_tc_supported(g)) {
       // the panel-column update (jhi == jlo + 1) runs beside the bulk update:
       // keep it narrow; the bulk update may be capped to leave SMs for the panel
       const int ctas = (jhi == jlo + 1) ? mt_opt_pcol_ctas() : mt_opt_update_ctas();

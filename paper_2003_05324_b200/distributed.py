@@ -1,25 +1,34 @@
-"""Multi-GPU likelihood evaluation: one process per GPU, NCCL panel broadcast.
+"""Multi-GPU likelihood evaluation: one process per GPU, 2D block-cyclic tiles.
 
-Layout: tile-column-cyclic (the 1 x g case of 2D block-cyclic): rank r stores
-tile columns j = r, r + g, r + 2g, ... in local pools (storage scales as 1/g,
-so full-DP N = 262144 fits on >= 2 B200s).  Step k of the right-looking
-factorization (factor.py:44-80) becomes, with lookahead 1 on two streams:
+Layout (north_star): a P x Q process grid, rank = r * Q + c;
+rank (r, c) stores the tiles (i, j) with i = r (mod P), j = c (mod Q) in
+local pools (storage ~1/(PQ) of the matrix: full DP at N = 262144 fits on
+2 B200s).  The reference's task DAG (factor.py:44-80) becomes, per step k:
 
-    owner(k+1), panel stream:  update(k -> column k+1), POTRF(k+1), TRSM(k+1)
-    everyone, panel stream:    broadcast panel k+1 from owner(k+1) (NCCL)
-    everyone, caller stream:   update(k -> owned columns k+2 .. p-1), which
-                               overlaps the panel chain and the broadcast and
-                               yields SMs to the panel kernels on request
+  owner of (k, k):        POTRF(k) [+ W = L_kk^{-1} for the tensor-core TRSM]
+  process column k%Q:     L_kk, its 32x32 inverses and W broadcast down the
+                          column (P > 1), then TRSM(k) of each rank's rows
+  every rank:             panel k's rows broadcast along process rows (each row
+                          operand A_ik reaches the ranks of row i%P), then down
+                          process columns (each column operand A_jk reaches the
+                          ranks of column j%Q)
+  every rank:             trailing update of its own tiles
 
-A panel is broadcast as the TF32 hi/lo split of its FP32 operands (rows
-k+1..p-1, what the tcgen05 update reads) plus its FP64 band rows (what the
-DMMA update reads), straight into every rank's panel ring.  Every tile
-receives the same updates in the same order from the same kernels as on one
-GPU, so factor, logdet and quad are bitwise identical for any rank count
-(tests/test_gpu_distributed.py).  logdet: per-diagonal-tile partials
-all-reduced (each entry has one non-zero contributor, so the sum is exact)
-then summed in fixed order; quad: forward sweep with the vector broadcast
-from each column owner, then the single-GPU reduction kernel.
+with lookahead 1 on two streams: the ranks of process column (k+1)%Q update
+tile column k+1 and factor panel k+1 on a high-priority panel stream while
+every rank applies step k to the rest of its tiles (yielding SMs to the panel
+kernels on request).  Panel rows travel as the TF32 hi/lo split of their FP32
+payload (what the tcgen05 update reads) plus FP64 rows for the band, in
+"ring order": tile row i sits at (i mod L) * ceil(p/L) + i // L, L = lcm(P, Q)
+(L = 1 on a 1 x Q grid), so every broadcast is one contiguous slice of a
+block of rows i = b (mod L).  Every tile receives the same updates in the
+same order from the same kernels as on one GPU, so the factor, logdet and
+quad are bitwise identical for any grid (tests/test_gpu_distributed.py,
+tests/test_distributed_cpu.py).  logdet: per-diagonal-tile partials,
+all-reduced (one non-zero contributor each: exact) and summed in fixed order;
+quad: the forward sweep y = L^{-1} z step by step -- TRSV on the owner of
+(i, i), y_i down process column i%Q, GEMV of each rank's rows, the updated x
+along process rows -- then y gathered exactly and reduced as on one GPU.
 """
 
 import ctypes
@@ -32,20 +41,75 @@ from .tilestore import PrecisionOverflowError, TileMatrix
 LOG_2PI = math.log(2.0 * math.pi)
 
 
+# --------------------------------------------------------------- grid plan
+def grid_shape(world, grid=None):
+    """(P, Q) of the process grid: `grid` if given, else 1 x world."""
+    if grid is None:
+        return 1, world
+    P, Q = int(grid[0]), int(grid[1])
+    if P < 1 or Q < 1 or P * Q != world:
+        raise ValueError(f"process grid {P}x{Q} does not match {world} ranks")
+    return P, Q
+
+
 def owner(j, world):
-    """Rank that stores tile column j."""
+    """Rank that stores tile column j on a 1 x world grid."""
     return j % world
 
 
-def schedule(p):
-    """Rank-independent action order of the distributed factorization (what
-    DistributedEvaluator.factor issues, the first three of each step on the
-    panel stream, the last on the caller stream).
+def tile_owner(i, j, P, Q):
+    """Rank storing tile (i, j) on a P x Q grid."""
+    return (i % P) * Q + (j % Q)
 
-    ("panel", k)            POTRF(k) + TRSM(k), executed by owner(k)
-    ("bcast", k)            panel k broadcast from owner(k) to every rank
-    ("update", k, jlo, jhi) step-k updates of each rank's owned columns in [jlo, jhi)
-    """
+
+def ring_geometry(p, P, Q):
+    """(L, rows per block, ring length) of the panel ring order (csrc/mt_grid.cuh)."""
+    L = 1 if P == 1 else P // math.gcd(P, Q) * Q
+    rq = -(-p // L)
+    return L, rq, L * rq
+
+
+def ring_pos(i, p, P, Q):
+    L, rq, _ = ring_geometry(p, P, Q)
+    return i if L == 1 else (i % L) * rq + i // L
+
+
+def panel_bcast_plan(k, p, P, Q, t):
+    """Broadcasts that distribute panel k, in issue order (the same on every rank).
+
+    Each entry is (stage, group, root, b, m0, m1, mb1): stage "row" runs in
+    process row `group` (root = the rank of column k%Q there), stage "col" in
+    process column `group` (root = the rank of row b%P there); block b holds
+    rows i = b + L*m, the broadcast covers m in [m0, m1] of the split ring and
+    m in [m0, mb1] of the FP64 ring (rows with i - k < t; mb1 < m0: none)."""
+    L, rq, _ = ring_geometry(p, P, Q)
+    out = []
+
+    def rng(b):
+        m0 = 0 if b > k else (k - b) // L + 1
+        m1 = (p - 1 - b) // L
+        mb1 = (min(k + t, p) - 1 - b) // L if min(k + t, p) - 1 >= b else -1
+        return m0, m1, mb1
+
+    if Q > 1:
+        for b in range(L):
+            m0, m1, mb1 = rng(b)
+            if m0 <= m1:
+                r = b % P
+                out.append(("row", r, r * Q + k % Q, b, m0, m1, mb1))
+    if P > 1:
+        for b in range(L):
+            m0, m1, mb1 = rng(b)
+            if m0 <= m1:
+                c = b % Q
+                out.append(("col", c, (b % P) * Q + c, b, m0, m1, mb1))
+    return out
+
+
+def schedule(p):
+    """Rank-independent action order of the 1 x g factorization (panel = POTRF +
+    TRSM on the column owner, bcast = its panel to every rank, update = step-k
+    updates of each rank's columns in [jlo, jhi))."""
     acts = [("panel", 0), ("bcast", 0)]
     for k in range(p - 1):
         acts += [("update", k, k + 1, k + 2), ("panel", k + 1), ("bcast", k + 1),
@@ -53,82 +117,144 @@ def schedule(p):
     return acts
 
 
-def panel_slices(m, k):
-    """(tensor view, description) pairs holding panel k in a rank's panel rings."""
-    p, te, t = m.p, m.nb * m.nb, m.policy.diag_thick
-    out = []
-    if m.split is not None and k + 1 < p:
-        base = ((k & 1) * p + k + 1) * 2 * te
-        out.append(m.split[base: ((k & 1) * p + p) * 2 * te])
-    rows = min(p, k + t) - (k + 1)  # band rows k+1 .. k+t-1
-    if rows > 0:
-        base = ((k & 1) * t + 1) * te
-        out.append(m.dpanel[base: base + rows * te])
-    return out
-
-
+# ------------------------------------------------------------- evaluator
 class DistributedEvaluator:
     """Likelihood evaluations of one dataset split over the ranks of `group`
-    (torch.distributed, NCCL on GPUs; gloo works for 1-GPU testing)."""
+    (torch.distributed, NCCL on GPUs; gloo works for 1-GPU testing) on a
+    P x Q process grid (`grid`, default 1 x world)."""
 
-    def __init__(self, assembler, policy, group=None):
+    def __init__(self, assembler, policy, group=None, grid=None):
         torch = _lib.require_cuda()
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.P, self.Q = grid_shape(self.world, grid)
+        self.pr, self.pc = divmod(self.rank, self.Q)
+        members = (dist.get_process_group_ranks(group) if group is not None
+                   else list(range(self.world)))
+        self.members = members
+        # sub-communicators: every rank creates every group, in the same order
+        self.row_groups, self.col_groups = [], []
+        if self.P > 1 and self.Q > 1:
+            self.row_groups = [dist.new_group([members[r * self.Q + c] for c in range(self.Q)])
+                               for r in range(self.P)]
+            self.col_groups = [dist.new_group([members[r * self.Q + c] for r in range(self.P)])
+                               for c in range(self.Q)]
+        elif self.Q > 1:
+            self.row_groups = [group]
+        elif self.P > 1:
+            self.col_groups = [group]
         self.asm = assembler
-        self.matrix = TileMatrix(assembler.n, assembler.nb, policy,
-                                 col_stride=self.world, col_offset=self.rank)
+        self.matrix = TileMatrix(assembler.n, assembler.nb, policy, col_stride=self.Q,
+                                 col_offset=self.pc, row_stride=self.P, row_offset=self.pr)
         m = self.matrix
         if self.world > 1 and (m.nb % 256 or (m.policy.mode.value == "mp" and m.split is None)):
             raise ValueError("the multi-GPU path needs nb % 256 == 0 (tcgen05 split panels)")
         dev = m.device
         npad = m.p * m.nb
         self.x = torch.empty(npad, dtype=torch.float64, device=dev)
+        self.y = torch.empty(npad, dtype=torch.float64, device=dev)
         self.partial = torch.empty(m.p, dtype=torch.float64, device=dev)
         self.work = torch.empty(2048, dtype=torch.float64, device=dev)
         self.out = torch.empty(1, dtype=torch.float64, device=dev)
         self.flag = torch.empty(3, dtype=torch.int64, device=dev)
         self.pan = torch.cuda.Stream(device=dev, priority=-1)
-        self.yield_sms = 32  # SMs the bulk update releases to the owner's panel kernels
+        self.yield_sms = 32  # SMs the bulk update releases to the panel kernels
 
-    # -- pieces -------------------------------------------------------------
-    def _bcast(self, k, async_op):
-        src = owner(k, self.world)
-        return [self.dist.broadcast(v, src=src, group=self.group, async_op=async_op)
-                for v in panel_slices(self.matrix, k)]
+    # -- helpers ------------------------------------------------------------
+    def _grank(self, r):
+        """Global rank (torch.distributed) of grid rank r."""
+        return self.members[r]
 
+    def _mine_col(self, k):
+        return k % self.Q == self.pc
+
+    def _mine_diag(self, k):
+        return k % self.P == self.pr and k % self.Q == self.pc
+
+    def _bcast(self, tensor, root, groups, index, async_op):
+        """Broadcast from grid rank `root` inside groups[index] (the whole
+        group when the grid is one row or one column)."""
+        return self.dist.broadcast(tensor, src=self._grank(root), group=groups[index],
+                                   async_op=async_op)
+
+    def _diag_bcast(self, k):
+        """L_kk (FP64 ring row k), its 32x32 inverses and W's split, down
+        process column k%Q from the owner of (k, k)."""
+        m, lib = self.matrix, _lib.load()
+        reg = (ctypes.c_int64 * 6)()
+        _lib.check(lib.mt_diag_regions(ctypes.byref(m.desc), k, reg), "mt_diag_regions")
+        root = (k % self.P) * self.Q + self.pc
+        views = [m.dpanel[reg[0]: reg[0] + reg[1]], m.scratch[reg[2]: reg[2] + reg[3]]]
+        if reg[5] > 0:
+            views.append(m.split[reg[4]: reg[4] + reg[5]])
+        for v in views:
+            if v.numel():
+                self._bcast(v, root, self.col_groups, 0 if self.Q == 1 else self.pc, False)
+
+    def _panel_bcast(self, k):
+        """Distribute panel k (panel_bcast_plan); returns the async handles."""
+        m = self.matrix
+        p, te, t = m.p, m.nb * m.nb, m.policy.diag_thick
+        L, rq, pring = ring_geometry(p, self.P, self.Q)
+        base = (k & 1) * pring
+        hs = []
+        for stage, grp, root, b, m0, m1, mb1 in panel_bcast_plan(k, p, self.P, self.Q, t):
+            if stage == "row":
+                if grp != self.pr:
+                    continue
+                groups, index = self.row_groups, (0 if self.P == 1 else grp)
+            else:
+                if grp != self.pc:
+                    continue
+                groups, index = self.col_groups, (0 if self.Q == 1 else grp)
+            r0 = base + b * rq
+            if m.split is not None:
+                v = m.split[(r0 + m0) * 2 * te: (r0 + m1 + 1) * 2 * te]
+                hs.append(self._bcast(v, root, groups, index, True))
+            if mb1 >= m0:
+                v = m.dpanel[(r0 + m0) * te: (r0 + mb1 + 1) * te]
+                hs.append(self._bcast(v, root, groups, index, True))
+        return hs
+
+    # -- factorization --------------------------------------------------------
     def factor(self):
         """The step loop with lookahead 1 on two streams (the single-GPU
-        schedule of csrc/api.cu, with the broadcast in the panel chain):
+        schedule of csrc/api.cu with the collectives in the panel chain):
 
-          panel stream (high priority): update(k -> column k+1) on its owner,
-                         POTRF+TRSM(k+1) on its owner, broadcast of panel k+1
-          caller stream: update(k -> owned columns k+2 ..), which yields SMs
-                         to the owner's panel kernels on request
+          panel stream (high priority): update(k -> column k+1) on the ranks of
+                         its process column, POTRF(k+1) on the owner of
+                         (k+1, k+1), the column broadcast of L, TRSM(k+1), the
+                         row/column broadcasts of panel k+1
+          caller stream: update(k -> this rank's columns k+2 ..), which yields
+                         SMs to the panel kernels on request
 
         The panel stream waits for the caller's step k-1 before touching the
-        panel ring slot of k+1 (= slot of k-1) and column k+1."""
+        ring slot of k+1 (= slot of k-1) and column k+1."""
         torch = _lib.require_cuda()
         m, lib = self.matrix, _lib.load()
         d = ctypes.byref(m.desc)
         main, pan = torch.cuda.current_stream(), self.pan
         hm, hp = ctypes.c_void_p(main.cuda_stream), ctypes.c_void_p(pan.cuda_stream)
-        mine = lambda k: owner(k, self.world) == self.rank  # noqa: E731
+        multi = self.world > 1
         bc = {}
 
         def panel(k):  # on the panel stream
-            if mine(k):
-                _lib.check(lib.mt_yield_request(self.yield_sms, hp), "mt_yield_request")
-                _lib.check(lib.mt_panel(d, k, hp), "mt_panel")
-                _lib.check(lib.mt_yield_request(0, hp), "mt_yield_request")
-            if self.world > 1:
-                with torch.cuda.stream(pan):
-                    bc[k] = self._bcast(k, async_op=True)
+            with torch.cuda.stream(pan):
+                if self._mine_col(k):
+                    _lib.check(lib.mt_yield_request(self.yield_sms, hp), "mt_yield_request")
+                    if self._mine_diag(k):
+                        _lib.check(lib.mt_panel_factor(d, k, hp), "mt_panel_factor")
+                    if self.P > 1:
+                        self._diag_bcast(k)
+                    _lib.check(lib.mt_panel_solve(d, k, hp), "mt_panel_solve")
+                    _lib.check(lib.mt_yield_request(0, hp), "mt_yield_request")
+                if multi:
+                    bc[k] = self._panel_bcast(k)
 
-        def received(k):  # the current stream waits for panel k's broadcast
+        def received(k):  # the current stream waits for panel k's broadcasts
             for h in bc.get(k, []):
                 h.wait()
 
@@ -139,7 +265,7 @@ class DistributedEvaluator:
             with torch.cuda.stream(pan):
                 if step_done is not None:
                     pan.wait_event(step_done)  # step k-1 applied everywhere on this rank
-                if mine(k + 1):
+                if self._mine_col(k + 1):
                     received(k)
                     _lib.check(lib.mt_update(d, k, k + 1, k + 2, hp), "mt_update")
             panel(k + 1)
@@ -179,17 +305,33 @@ class DistributedEvaluator:
         return 2.0 * tot
 
     def quad(self):
+        """||L^{-1} z||^2: forward sweep by owner (see the module docstring)."""
         m, lib, st = self.matrix, _lib.load(), _lib.stream_handle()
-        self.x.copy_(self.asm.d_z)
-        nb = m.nb
+        d = ctypes.byref(m.desc)
+        x = self.x
+        x.copy_(self.asm.d_z)
+        nb, P, Q = m.nb, self.P, self.Q
         for i in range(m.p):
-            if owner(i, self.world) == self.rank:
-                _lib.check(lib.mt_fwd_step(ctypes.byref(m.desc), i, _lib.ptr(self.x), st),
-                           "mt_fwd_step")
-            if self.world > 1:
-                self.dist.broadcast(self.x[i * nb:], src=owner(i, self.world), group=self.group)
-        _lib.check(lib.mt_sumsq(_lib.ptr(self.x), self.x.numel(), _lib.ptr(self.work),
-                                _lib.ptr(self.out), st), "mt_sumsq")
+            if self._mine_diag(i):
+                _lib.check(lib.mt_fwd_step_ex(d, i, 1, _lib.ptr(x), st), "mt_fwd_step_ex")
+            if self._mine_col(i):
+                if P > 1:
+                    self._bcast(x[i * nb:(i + 1) * nb], (i % P) * Q + self.pc, self.col_groups,
+                                0 if Q == 1 else self.pc, False)
+                _lib.check(lib.mt_fwd_step_ex(d, i, 2, _lib.ptr(x), st), "mt_fwd_step_ex")
+            if Q > 1 and i + 1 < m.p:
+                self._bcast(x[(i + 1) * nb:], self.pr * Q + i % Q, self.row_groups,
+                            0 if P == 1 else self.pr, False)
+        # y_i lives on the owner of (i, i): gather exactly (one non-zero term each)
+        y = self.y
+        y.zero_()
+        for i in range(m.p):
+            if self._mine_diag(i):
+                y[i * nb:(i + 1) * nb] = x[i * nb:(i + 1) * nb]
+        if self.world > 1:
+            self.dist.all_reduce(y, group=self.group)
+        _lib.check(lib.mt_sumsq(_lib.ptr(y), y.numel(), _lib.ptr(self.work), _lib.ptr(self.out),
+                                st), "mt_sumsq")
         return float(self.out.item())
 
     def __call__(self, params, chol_events=None):
@@ -212,10 +354,10 @@ class DistributedEvaluator:
         return self.logdet(), self.quad()
 
 
-def loglik_distributed(dataset, params, nb, policy, group=None):
+def loglik_distributed(dataset, params, nb, policy, group=None, grid=None):
     """Distributed counterpart of mle.loglik (mle.py:89-99); call on every rank."""
     from .mle import LikelihoodEval
     from .tilestore import TileAssembler
-    ev = DistributedEvaluator(TileAssembler(dataset, nb), policy, group)
+    ev = DistributedEvaluator(TileAssembler(dataset, nb), policy, group, grid)
     ld, quad = ev(params)
     return LikelihoodEval(-0.5 * (dataset.n * LOG_2PI + ld + quad), ld, quad)

@@ -109,7 +109,8 @@ class _TileView(Mapping):
         m = self._m
         for j in range(m.col_offset, m.p, m.col_stride):  # owned tile columns
             for i in range(j, m.p):
-                if m.policy.mode.value != "dst" or i - j < m.policy.diag_thick:
+                if (i - m.row_offset) % m.row_stride == 0 and (
+                        m.policy.mode.value != "dst" or i - j < m.policy.diag_thick):
                     yield (i, j)
 
     def __iter__(self):
@@ -125,7 +126,8 @@ class _TileView(Mapping):
             return False
         m = self._m
         return (0 <= j <= i < m.p and (j - m.col_offset) % m.col_stride == 0
-                and j >= m.col_offset
+                and j >= m.col_offset and i >= m.row_offset
+                and (i - m.row_offset) % m.row_stride == 0
                 and (m.policy.mode.value != "dst" or i - j < m.policy.diag_thick))
 
     def __getitem__(self, key):
@@ -146,7 +148,8 @@ class TileMatrix:
     here (use `from_dense` to upload explicit payloads).
     """
 
-    def __init__(self, n, nb, policy, device=None, col_stride=1, col_offset=0):
+    def __init__(self, n, nb, policy, device=None, col_stride=1, col_offset=0, row_stride=1,
+                 row_offset=0):
         if n < 1:
             raise ValueError(f"need n >= 1, got {n}")
         if nb < 1:
@@ -159,26 +162,31 @@ class TileMatrix:
         self.duplicate_locations = False
         self.factored = False
         self._version = 0
-        # multi-GPU: this rank stores tile columns col_offset + m * col_stride only
+        # multi-GPU, P x Q block-cyclic: this rank stores the tiles (i, j) with
+        # j = col_offset (mod col_stride = Q) and i = row_offset (mod row_stride = P)
         self.col_stride, self.col_offset = int(col_stride), int(col_offset)
+        self.row_stride, self.row_offset = int(row_stride), int(row_offset)
+        multi = self.col_stride > 1 or self.row_stride > 1
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         lib = _lib.load()
         mode = _lib.MODE_CODE[self.policy.mode.value]
         t = self.policy.diag_thick
         te = self.nb * self.nb
         ndp, nsp = ctypes.c_int64(), ctypes.c_int64()
-        lib.mt_local_tiles(self.p, t, mode, self.col_stride, self.col_offset,
-                           ctypes.byref(ndp), ctypes.byref(nsp))
+        lib.mt_local_tiles_ex(self.p, t, mode, self.row_stride, self.row_offset, self.col_stride,
+                              self.col_offset, ctypes.byref(ndp), ctypes.byref(nsp))
         ndp, nsp = ndp.value, nsp.value
         nsc = lib.mt_scratch_tiles(self.p, t, mode, self.nb)
-        nsl = lib.mt_split_tiles(self.p, t, mode) if self.nb % 256 == 0 else 0
+        nsl = (lib.mt_split_tiles_ex(self.p, t, mode, self.row_stride, self.col_stride)
+               if self.nb % 256 == 0 else 0)
         self.dp_pool = torch.empty(max(ndp, 1) * te, dtype=torch.float64, device=dev)
         self.sp_pool = torch.empty(max(nsp, 1) * te, dtype=torch.float32, device=dev)
         self.scratch = torch.empty(max(nsc, 1) * te, dtype=torch.float32, device=dev)
         self.split = (torch.empty(nsl * te, dtype=torch.float32, device=dev) if nsl else None)
         self.dpanel = None
-        if self.col_stride > 1:
-            self.dpanel = torch.empty(lib.mt_dpanel_tiles(self.p, t, mode) * te,
+        if multi:
+            self.dpanel = torch.empty(lib.mt_dpanel_tiles_ex(self.p, self.row_stride,
+                                                             self.col_stride) * te,
                                       dtype=torch.float64, device=dev)
         self.status = torch.empty(4, dtype=torch.int64, device=dev)
         self.desc = _lib.MtTiles(self.n, self.nb, self.p, t, mode, self.dp_pool.data_ptr(),
@@ -186,7 +194,8 @@ class TileMatrix:
                                  self.status.data_ptr(),
                                  self.split.data_ptr() if self.split is not None else 0,
                                  self.col_stride, self.col_offset,
-                                 self.dpanel.data_ptr() if self.dpanel is not None else 0)
+                                 self.dpanel.data_ptr() if self.dpanel is not None else 0,
+                                 self.row_stride, self.row_offset)
         self.reset_status()
         self.tiles = _TileView(self)
 

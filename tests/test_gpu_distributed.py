@@ -1,6 +1,6 @@
 """GPU: the multi-GPU path (distributed.DistributedEvaluator) end to end.
 
-The gpurun box has one B200, so two ranks share cuda:0 and talk over gloo
+The gpurun box has one B200, so the ranks share cuda:0 and talk over gloo
 (NCCL refuses two ranks on one device); the CUDA kernels, local pools,
 panel rings and the step schedule are the ones a multi-GPU NCCL run uses.
 Factor tiles, logdet and quad must be bitwise identical to one GPU.
@@ -27,7 +27,7 @@ def _data(n):
     return g["locs"][:n], g["z"][:n]
 
 
-def _worker(rank, world, port, n, nb, tag, queue):
+def _worker(rank, world, port, n, nb, tag, queue, grid=None):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -38,26 +38,32 @@ def _worker(rank, world, port, n, nb, tag, queue):
     locs, z = _data(n)
     ds = mt.GeoDataset(locs, z)
     pol = mt.PrecisionPolicy.dp() if tag == "dp" else mt.PrecisionPolicy.mp(diag_thick=int(tag[3:]))
-    ev = DistributedEvaluator(mt.TileAssembler(ds, nb), pol)
+    ev = DistributedEvaluator(mt.TileAssembler(ds, nb), pol, grid=grid)
     ld, quad = ev(mt.MaternParams(1.0, 0.1, 0.5))
     tiles = {key: (t.dp, t.sp) for key, t in ev.matrix.tiles.items()}
     queue.put((rank, ld, quad, tiles))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("tag", ["mp:2", "dp", "mp:1"])
-def test_two_ranks_bitwise_equal_single_gpu(gpu, tag):
+@pytest.mark.parametrize("tag,grid", [("mp:2", (1, 2)), ("dp", (1, 2)), ("mp:1", (1, 2)),
+                                      ("mp:2", (2, 2)), ("dp", (2, 2)), ("mp:3", (2, 1)),
+                                      ("mp:2", (2, 1))])
+def test_ranks_bitwise_equal_single_gpu(gpu, tag, grid):
+    """1 x 2, 2 x 1 and 2 x 2 process grids (2D block-cyclic tiles, row and
+    column sub-communicators): factor, logdet and quad bitwise equal to one GPU."""
     import sys
     import torch.multiprocessing as mp
     import paper_2003_05324_b200 as mt
-    n, nb, world = 2048, 256, 2
+    n, nb = 2048, 256
+    world = grid[0] * grid[1]
     here = os.path.dirname(os.path.abspath(__file__))
     if here not in sys.path:
         sys.path.insert(0, here)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, nb, tag, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, nb, tag, q, grid))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=600) for _ in range(world)]
@@ -78,5 +84,6 @@ def test_two_ranks_bitwise_equal_single_gpu(gpu, tag):
                 assert np.array_equal(sp, r.sp), (rank, key)
             else:
                 assert np.array_equal(dp, r.dp), (rank, key)
+            assert key not in seen, key  # every tile stored by exactly one rank
             seen.add(key)
     assert seen == set(ref)
