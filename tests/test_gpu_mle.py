@@ -150,6 +150,12 @@ def test_evaluate_host_c_entry(gpu):
     want = g["results"]["mp:2"]
     assert math.isclose(out[0], want[1], rel_tol=1e-6)
     assert math.isclose(out[1], want[2], rel_tol=1e-5)
+    # the C entry point allocates the split buffer and runs the production
+    # engine (the tcgen05 kernels), so it agrees with the Python path bitwise
+    ev = mt.Evaluator(mt.TileAssembler(mt.GeoDataset(g["locs"], g["z"]), 256),
+                      mt.PrecisionPolicy.mp(diag_thick=2))
+    ld, quad = ev(mt.MaternParams(*g["theta"]))
+    assert (out[0], out[1]) == (ld, quad)
 
 
 def test_evaluator_split_launch_equals_fused(gpu):
