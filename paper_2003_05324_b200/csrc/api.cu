@@ -249,6 +249,7 @@ static int g_wide_l2pf = 0;    // 1 = the 256 x 512 update stages each warp's C 
 static int g_cta_pairs = 1;    // 1 = FP32 update/TRSM on CTA pairs (tcgen05 cta_group::2)
 static int g_tc_diag = 0;      // diagnostics (wrong results): 1 no C loads, 2 no C stores, 4 no epilogue
 static int g_c_prefetch = 0;   // 1 = FP32 update stages each item's C block in L2 (cp.async.bulk.prefetch)
+static int g_potrf_cluster = 1;  // 1 = POTRF on a cluster of nb/32 CTAs (tile in distributed smem)
 int mt_opt_engine() { return g_engine; }
 int mt_opt_update_ctas() { return g_update_ctas; }
 int mt_opt_legacy_dmma() { return g_legacy_dmma; }
@@ -263,6 +264,7 @@ int mt_opt_wide_items() { return g_wide_items; }
 int mt_opt_wide_l2pf() { return g_wide_l2pf; }
 int mt_opt_coschedule() { return g_coschedule; }
 int mt_opt_coschedule_pct() { return g_cosched_pct; }
+int mt_opt_potrf_cluster() { return g_potrf_cluster; }
 
 extern "C" {
 
@@ -299,6 +301,7 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 11) { old = g_cosched_pct; g_cosched_pct = value; }
   else if (option == 12) { old = g_wide_items; g_wide_items = value; }
   else if (option == 13) { old = g_wide_l2pf; g_wide_l2pf = value; }
+  else if (option == 14) { old = g_potrf_cluster; g_potrf_cluster = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

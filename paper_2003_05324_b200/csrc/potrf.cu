@@ -15,6 +15,8 @@
 // inverses (FP64 + FP32) are kept for the panel TRSM, and in MP mode the
 // factor is narrowed to FP32 for the off-band panel solves (sp_diag,
 // factor.py:255-256).  The strict upper triangle is never written.
+#include <cooperative_groups.h>
+
 #include "mt_grid.cuh"
 
 namespace {
@@ -217,18 +219,221 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int n
   //  finalised; the TRSM never reads the strict upper part)
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster POTRF: the tile's 32-row blocks spread over a thread-block cluster
+// of nb/32 CTAs (one SM each), the tile resident in distributed shared memory.
+// CTA c holds row block c (its 32 x 32(c+1) lower part).  For each column
+// block cb: CTA cb factors its diagonal block and forms the inverse (the same
+// warp-shuffle pivots and CTA inverse as potrf_kernel); after a cluster
+// barrier every CTA c > cb solves its panel block X_c = A[c,cb] Li^T; after a
+// second barrier it applies A[c,q] -= X_c X_q^T for cb < q <= c on DMMA,
+// reading X_q from CTA q's shared memory.  Every element sees the same
+// operations in the same order as in potrf_kernel (panel FMAs in q order,
+// SYRK blocks accumulated k4-ascending then subtracted once): bitwise equal
+// results, with the serial chain cut from ~1.4 ms to the diagonal-block work
+// plus 2 cluster barriers per column block.
+namespace cg = cooperative_groups;
+constexpr int CLD = 8;  // row padding (doubles) of the resident row block
+
+__global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int k, int narrow) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int c = (int)cluster.block_rank();  // this CTA's row block
+  const int nblk = (int)cluster.num_blocks();
+  const int nb = g.nb;
+  const int ld = nb + CLD;                  // resident rows: 32 x ld doubles
+  extern __shared__ __align__(16) double R[];   // [32][ld]: rows 32c.. of the tile
+  double* Ld = R + 32 * ld;                      // [32][33] diagonal factor (owner)
+  double* Li = Ld + 32 * 33;                     // [32][33] its inverse (owner)
+  double* Lp = Li + 32 * 33;                     // [32][33] peer's inverse (copy)
+  double* Xq = Lp + 32 * 33;                     // [32][36] peer's panel block (copy)
+  __shared__ int bad;
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* A = g.dtile(k, k);
+  double* inv64 = g.sinv64(k);
+  float* inv32 = g.sinv32(k);
+  if (threadIdx.x == 0) bad = -1;
+  const bool failed0 = g.failed();
+  // load the lower part of row block c (columns 0 .. 32(c+1)-1)
+  const int wcols = 32 * (c + 1);
+  for (int e = threadIdx.x; e < 32 * wcols; e += kThreads) {
+    const int r = e / wcols, q = e % wcols;
+    R[r * ld + q] = A[(int64_t)(32 * c + r) * nb + q];
+  }
+  cluster.sync();
+  if (failed0) return;  // uniform: every CTA read the same status word
+
+  for (int cb = 0; cb < nblk; ++cb) {
+    double* Dcb = R + cb * 32;  // block (c, cb) of this CTA's rows
+    if (c == cb) {
+      // -------- diagonal block: warp 0 factors it in registers (potrf_kernel step 1)
+      if (warp == 0) {
+        const int r = lane;
+        double a[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) a[q] = q <= r ? Dcb[r * ld + q] : 0.0;
+        int fail = -1;
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j) {
+          double piv = __shfl_sync(0xffffffffu, a[0], j);
+          if (fail < 0 && !(piv > 0.0)) fail = j;
+          if (fail >= 0) piv = 1.0;
+          const double d = sqrt(piv);
+          double lrj = a[0];
+          if (r == j) lrj = d;
+          else if (r > j) lrj = lrj / d;
+          Ld[r * 33 + j] = r >= j ? lrj : 0.0;
+#pragma unroll
+          for (int cc = 1; cc < 32; ++cc) {
+            const double lcj = __shfl_sync(0xffffffffu, lrj, (j + cc) & 31);
+            if (j + cc < 32 && r >= j + cc) a[cc] -= lrj * lcj;
+          }
+#pragma unroll
+          for (int cc = 0; cc < 31; ++cc) a[cc] = a[cc + 1];
+          a[31] = 0.0;
+        }
+        if (fail >= 0 && lane == 0) bad = cb * 32 + fail;
+      }
+      __syncthreads();
+      if (bad < 0) {
+        const int ci = threadIdx.x & 31, pt = threadIdx.x >> 5;
+#pragma unroll 1
+        for (int r = 0; r < 32; ++r) {
+          double sacc = 0.0;
+          for (int q = ci + pt; q < r; q += 8) sacc += Ld[r * 33 + q] * Li[q * 33 + ci];
+          part[pt][ci] = sacc;
+          __syncthreads();
+          if (pt == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t += part[u][ci];
+            Li[r * 33 + ci] = r < ci ? 0.0 : (r == ci ? 1.0 / Ld[r * 33 + r] : -t / Ld[r * 33 + r]);
+          }
+          __syncthreads();
+        }
+        for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
+          const int r = e >> 5, q = e & 31;
+          if (q <= r) Dcb[r * ld + q] = Ld[r * 33 + q];
+          inv64[cb * 1024 + e] = Li[r * 33 + q];
+          inv32[cb * 1024 + e] = __double2float_rn(Li[r * 33 + q]);
+        }
+      } else if (threadIdx.x == 0) {
+        atomicCAS((unsigned long long*)&g.status[MT_ST_PIVOT], (unsigned long long)-1LL,
+                  (unsigned long long)((int64_t)k * nb + bad));
+      }
+    }
+    cluster.sync();  // (1) diagonal block cb and its inverse are final
+    const int fail = *cluster.map_shared_rank(&bad, cb);
+    if (fail >= 0) return;  // uniform across the cluster
+    if (c > cb) {
+      // -------- panel block: X = A[c, cb] Li^T (potrf_kernel step 2)
+      const double* Lr = cluster.map_shared_rank(Li, cb);
+      for (int e = threadIdx.x; e < 32 * 32; e += kThreads) Lp[(e >> 5) * 33 + (e & 31)] = Lr[(e >> 5) * 33 + (e & 31)];
+      __syncthreads();
+      const int rr = threadIdx.x >> 3, cg4 = (threadIdx.x & 7) * 4;
+      double o[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+      for (int q = 0; q < 32; ++q) {
+        const double av = Dcb[rr * ld + q];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] += av * Lp[(cg4 + u) * 33 + q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) Dcb[rr * ld + cg4 + u] = o[u];
+    }
+    cluster.sync();  // (2) panel blocks of column cb are final
+    if (c > cb) {
+      // -------- trailing blocks of row block c: A[c, q] -= X_c X_q^T (DMMA)
+      for (int q = cb + 1; q <= c; ++q) {
+        const double* Xsrc = q == c ? Dcb : cluster.map_shared_rank(R, q) + cb * 32;
+        __syncthreads();  // Xq free (previous q consumed)
+        for (int e = threadIdx.x; e < 32 * 32; e += kThreads)
+          Xq[(e >> 5) * 36 + (e & 31)] = Xsrc[(e >> 5) * ld + (e & 31)];
+        __syncthreads();
+        // 16 fragments of 8 x 8, two per warp
+        const int fm = warp >> 1, fn0 = (warp & 1) * 2;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int k4 = 0; k4 < 32; k4 += 4) {
+          const double af = Dcb[(fm * 8 + (lane >> 2)) * ld + k4 + (lane & 3)];
+#pragma unroll
+          for (int f = 0; f < 2; ++f) {
+            const double bf = Xq[((fn0 + f) * 8 + (lane >> 2)) * 36 + k4 + (lane & 3)];
+            dmma884(acc[f], af, bf);
+          }
+        }
+        double* Cq = R + q * 32;
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          const int r = fm * 8 + (lane >> 2), col = (fn0 + f) * 8 + 2 * (lane & 3);
+          Cq[r * ld + col] -= acc[f][0];
+          Cq[r * ld + col + 1] -= acc[f][1];
+        }
+      }
+    }
+  }
+  cluster.sync();  // peers no longer read this CTA's blocks
+  // write back the lower part of row block c and its FP32 narrowing
+  float* S = narrow ? g.sdiag(k) : nullptr;
+  for (int e = threadIdx.x; e < 32 * wcols; e += kThreads) {
+    const int r = e / wcols, q = e % wcols;
+    if (q > 32 * c + r) continue;  // strict upper part of the diagonal block
+    const int64_t o = (int64_t)(32 * c + r) * nb + q;
+    const double v = R[r * ld + q];
+    A[o] = v;
+    if (S) S[o] = __double2float_rn(v);
+  }
+}
+
 }  // namespace
 
+static size_t potrf_cluster_smem(int nb) {
+  return ((size_t)32 * (nb + CLD) + 3 * 32 * 33 + 32 * 36) * sizeof(double);
+}
+
+// cluster kernel when the tile splits into 2..16 row blocks of 32 and fits in
+// distributed shared memory; the single-CTA kernel otherwise (same results)
+static int g_potrf_cluster = -1;  // -1 unknown, 0 unavailable, 1 usable
+
 int mt_potrf_impl(const Grid& g, int k, int narrow, cudaStream_t st) {
+  const double r = g.rows(k);
+  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0,
+               (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)));
+  const int nblk = g.nb / 32;
+  if (mt_opt_potrf_cluster() && g.nb % 32 == 0 && nblk >= 2 && nblk <= 16 &&
+      potrf_cluster_smem(g.nb) <= 220 * 1024 && g_potrf_cluster != 0) {
+    const size_t smem = potrf_cluster_smem(g.nb);
+    cudaFuncSetAttribute(potrf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(potrf_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = nblk;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, potrf_cluster_kernel, g, k, narrow);
+    if (e == cudaSuccess) {
+      g_potrf_cluster = 1;
+      return MT_OK;
+    }
+    if (g_potrf_cluster == 1) return mt_cuda_check(e, "potrf_cluster_kernel") ? MT_E_CUDA : MT_OK;
+    cudaGetLastError();  // first use: cluster shape unsupported here -> single-CTA kernel
+    g_potrf_cluster = 0;
+  }
   const size_t smem = (size_t)(g.nb > 32 ? g.nb - 32 : 1) * PLD * sizeof(double);
   if (smem > 200 * 1024) {
     mt_set_error("potrf: nb=%d exceeds the supported maximum", g.nb);
     return MT_E_BAD_ARG;
   }
   cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const double r = g.rows(k);
-  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0,
-               (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)));
   potrf_kernel<<<1, kThreads, smem, st>>>(g, k, narrow);
   MT_LAUNCH_CHECK("potrf_kernel");
   return MT_OK;

@@ -26,9 +26,10 @@ same order from the same kernels as on one GPU, so the factor, logdet and
 quad are bitwise identical for any grid (tests/test_gpu_distributed.py,
 tests/test_distributed_cpu.py).  logdet: per-diagonal-tile partials,
 all-reduced (one non-zero contributor each: exact) and summed in fixed order;
-quad: the forward sweep y = L^{-1} z step by step -- TRSV on the owner of
-(i, i), y_i down process column i%Q, GEMV of each rank's rows, the updated x
-along process rows -- then y gathered exactly and reduced as on one GPU.
+quad: the forward sweep y = L^{-1} z fused into the schedule, step i on the
+panel stream right after panel i -- TRSV on the owner of (i, i), y_i down
+process column i%Q, GEMV of each rank's rows, the updated x along process
+rows -- then y gathered exactly and reduced as on one GPU.
 """
 
 import ctypes
@@ -240,6 +241,21 @@ class DistributedEvaluator:
         hm, hp = ctypes.c_void_p(main.cuda_stream), ctypes.c_void_p(pan.cuda_stream)
         multi = self.world > 1
         bc = {}
+        x, nb, P, Q = self.x, m.nb, self.P, self.Q
+        x.copy_(self.asm.d_z)  # the forward sweep of quad runs fused into the schedule
+
+        def fwd(i):  # forward-sweep step i on the panel stream, right after panel i
+            with torch.cuda.stream(pan):
+                if self._mine_diag(i):
+                    _lib.check(lib.mt_fwd_step_ex(d, i, 1, _lib.ptr(x), hp), "mt_fwd_step_ex")
+                if self._mine_col(i):
+                    if P > 1:
+                        self._bcast(x[i * nb:(i + 1) * nb], (i % P) * Q + self.pc,
+                                    self.col_groups, 0 if Q == 1 else self.pc, False)
+                    _lib.check(lib.mt_fwd_step_ex(d, i, 2, _lib.ptr(x), hp), "mt_fwd_step_ex")
+                if Q > 1 and i + 1 < m.p:
+                    self._bcast(x[(i + 1) * nb:], self.pr * Q + i % Q, self.row_groups,
+                                0 if P == 1 else self.pr, False)
 
         def panel(k):  # on the panel stream
             with torch.cuda.stream(pan):
@@ -258,8 +274,9 @@ class DistributedEvaluator:
             for h in bc.get(k, []):
                 h.wait()
 
-        pan.wait_stream(main)  # generation of the local tiles
+        pan.wait_stream(main)  # generation of the local tiles, x = z
         panel(0)
+        fwd(0)
         step_done = None
         for k in range(m.p - 1):
             with torch.cuda.stream(pan):
@@ -269,6 +286,7 @@ class DistributedEvaluator:
                     received(k)
                     _lib.check(lib.mt_update(d, k, k + 1, k + 2, hp), "mt_update")
             panel(k + 1)
+            fwd(k + 1)
             received(k)
             bc.pop(k, None)
             if k + 2 < m.p:
@@ -305,25 +323,12 @@ class DistributedEvaluator:
         return 2.0 * tot
 
     def quad(self):
-        """||L^{-1} z||^2: forward sweep by owner (see the module docstring)."""
+        """||L^{-1} z||^2 after factor(): the forward sweep ran inside the
+        schedule (see the module docstring); y_i lives on the owner of (i, i),
+        gathered exactly (one non-zero term per entry) and reduced in the
+        single-GPU order."""
         m, lib, st = self.matrix, _lib.load(), _lib.stream_handle()
-        d = ctypes.byref(m.desc)
-        x = self.x
-        x.copy_(self.asm.d_z)
-        nb, P, Q = m.nb, self.P, self.Q
-        for i in range(m.p):
-            if self._mine_diag(i):
-                _lib.check(lib.mt_fwd_step_ex(d, i, 1, _lib.ptr(x), st), "mt_fwd_step_ex")
-            if self._mine_col(i):
-                if P > 1:
-                    self._bcast(x[i * nb:(i + 1) * nb], (i % P) * Q + self.pc, self.col_groups,
-                                0 if Q == 1 else self.pc, False)
-                _lib.check(lib.mt_fwd_step_ex(d, i, 2, _lib.ptr(x), st), "mt_fwd_step_ex")
-            if Q > 1 and i + 1 < m.p:
-                self._bcast(x[(i + 1) * nb:], self.pr * Q + i % Q, self.row_groups,
-                            0 if P == 1 else self.pr, False)
-        # y_i lives on the owner of (i, i): gather exactly (one non-zero term each)
-        y = self.y
+        nb, x, y = m.nb, self.x, self.y
         y.zero_()
         for i in range(m.p):
             if self._mine_diag(i):

@@ -274,3 +274,52 @@ def test_fused_forward_sweep_bitwise(gpu, n, nb, t, la):
         torch.cuda.synchronize()
         outs.append(float(out.item()))
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("n,nb,pol", [(4096, 512, "mp:2"), (3000, 256, "dp"), (2048, 64, "mp:3"),
+                                      (1920, 128, "dst:2")])
+def test_cluster_potrf_bitwise_equals_single_cta(gpu, n, nb, pol):
+    """Option 14: POTRF on a cluster of nb/32 CTAs (tile in distributed shared
+    memory) applies the single-CTA kernel's operations in the same order: the
+    factor (including the FP32 narrowing and the 32x32 inverses feeding the
+    TRSM) is bitwise identical; ragged last tile included."""
+    import paper_2003_05324_b200 as mt
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    locs = mt.generate_locations(n, seed=41)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    mode, _, t = pol.partition(":")
+    policy = (mt.PrecisionPolicy.dp() if mode == "dp" else
+              getattr(mt.PrecisionPolicy, mode)(diag_thick=int(t)))
+    facs = []
+    for flag in (0, 1):
+        old = lib.mt_set_option(14, flag)
+        try:
+            facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), nb,
+                                                           policy)))
+        finally:
+            lib.mt_set_option(14, old)
+    for key in facs[0].tiles:
+        a, b = facs[0].tiles[key], facs[1].tiles[key]
+        assert np.array_equal(a.dp, b.dp), key
+        assert (a.sp is None) == (b.sp is None) and (a.sp is None or np.array_equal(a.sp, b.sp))
+
+
+def test_cluster_potrf_not_positive_definite_index(gpu):
+    """The cluster POTRF reports the same global pivot as the reference."""
+    import paper_2003_05324_b200 as mt
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    n, nb = 1024, 256
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, n))
+    a = x @ x.T / n + np.eye(n)
+    a[600, 600] = -5.0
+    for flag in (0, 1):
+        old = lib.mt_set_option(14, flag)
+        try:
+            with pytest.raises(mt.FactorizationError) as exc:
+                mt.cholesky(mt.TileMatrix.from_dense(a, nb, mt.PrecisionPolicy.dp()))
+            assert exc.value.index == 600
+        finally:
+            lib.mt_set_option(14, old)
