@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int 
 
   for (int cb = 0; cb < nblk; ++cb) {
     double* Dcb = R + cb * 32;  // block (c, cb) of this CTA's rows
+    __syncthreads();  // the previous step's trailing writes (all warps) before the diagonal read
     if (c == cb) {
       // -------- diagonal block: warp 0 factors it in registers (potrf_kernel step 1)
       if (warp == 0) {
@@ -325,7 +326,10 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int 
     }
     cluster.sync();  // (1) diagonal block cb and its inverse are final
     const int fail = *cluster.map_shared_rank(&bad, cb);
-    if (fail >= 0) return;  // uniform across the cluster
+    if (fail >= 0) {  // uniform across the cluster
+      cluster.sync();  // nobody exits while a peer may still read its shared memory
+      return;
+    }
     if (c > cb) {
       // -------- panel block: X = A[c, cb] Li^T (potrf_kernel step 2)
       const double* Lr = cluster.map_shared_rank(Li, cb);
