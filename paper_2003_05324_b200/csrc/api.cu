@@ -249,7 +249,7 @@ static int g_wide_l2pf = 0;    // 1 = the 256 x 512 update stages each warp's C 
 static int g_cta_pairs = 1;    // 1 = FP32 update/TRSM on CTA pairs (tcgen05 cta_group::2)
 static int g_tc_diag = 0;      // diagnostics (wrong results): 1 no C loads, 2 no C stores, 4 no epilogue
 static int g_c_prefetch = 0;   // 1 = FP32 update stages each item's C block in L2 (cp.async.bulk.prefetch)
-static int g_potrf_cluster = 1;  // 1 = POTRF on a cluster of nb/32 CTAs (tile in distributed smem)
+static int g_potrf_cluster = 0;  // 1 = POTRF on a cluster of nb/32 CTAs (tile in distributed smem; opt-in)
 int mt_opt_engine() { return g_engine; }
 int mt_opt_update_ctas() { return g_update_ctas; }
 int mt_opt_legacy_dmma() { return g_legacy_dmma; }

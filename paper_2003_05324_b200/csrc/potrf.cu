@@ -231,8 +231,11 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int n
 // reading X_q from CTA q's shared memory.  Every element sees the same
 // operations in the same order as in potrf_kernel (panel FMAs in q order,
 // SYRK blocks accumulated k4-ascending then subtracted once): bitwise equal
-// results, with the serial chain cut from ~1.4 ms to the diagonal-block work
-// plus 2 cluster barriers per column block.
+// results (tests/test_gpu_factor.py).  Alone it takes 0.75 ms per 512-tile
+// against 1.37 ms (ncu); inside the factorization it is slower overall (862 ->
+// 1100 ms Cholesky at N=65536): the 16-CTA cluster must find a whole GPC free
+// beside the co-scheduled bulk update, stalling the panel chain.  Opt-in
+// (option 14) for layouts where the panel chain is exposed.
 namespace cg = cooperative_groups;
 constexpr int CLD = 8;  // row padding (doubles) of the resident row block
 

@@ -69,3 +69,33 @@ def test_config2_solve_round_trip(field65536):
     assert np.max(np.abs(back - ds.z)) <= 1e-9 * np.max(np.abs(ds.z)) * 1e3
     x = mt.solve(fac, ds.z)                # Sigma^{-1} z; z.x = ||L^{-1} z||^2
     assert math.isclose(float(ds.z @ x), float(y @ y), rel_tol=1e-9)
+
+
+def test_config2_parity_vs_cpu_reference(gpu):
+    """configs[1] size against the CPU reference (oracle port, bitwise-pinned
+    on the small goldens): the same N=65536 field (GPU full-DP generate_field
+    z, tests/golden/field65536.npz, tools/golden65536_cpu.py), DP to 1e-8 and
+    MP at t=2 / t=8 to 1e-5 (north_star); the GPU's MP is no further from DP
+    than the reference's MP (1.5x noise margin)."""
+    from conftest import load_golden
+    mt = _mt()
+    g = load_golden("field65536")
+    n = len(g["z"])
+    locs = mt.generate_locations(n, seed=mt.derive_seed(2, 0))
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    ds = mt.GeoDataset(ds.locations, g["z"])
+    th = mt.MaternParams(*(float(v) for v in g["theta"]))
+    cpu = g["results"]
+    l_dp = cpu["dp"][0]
+    for tag, tol in (("dp", 1e-8), ("mp:2", 1e-5), ("mp:8", 1e-5)):
+        pol = mt.PrecisionPolicy.dp() if tag == "dp" else mt.PrecisionPolicy.mp(
+            diag_thick=int(tag.split(":")[1]))
+        ev = mt.loglik(ds, th, 512, pol)
+        want = cpu[tag][0]
+        rel = abs(ev.value - want) / abs(want)
+        print(f"field65536 {tag}: GPU {ev.value!r} CPU {want!r} rel {rel:.2e}")
+        assert rel <= tol, (tag, ev.value, want, rel)
+        if tag != "dp":
+            gpu_gap = abs(ev.value - l_dp) / abs(l_dp)
+            cpu_gap = abs(want - l_dp) / abs(l_dp)
+            assert gpu_gap <= 1.5 * cpu_gap + 1e-9, (tag, gpu_gap, cpu_gap)
