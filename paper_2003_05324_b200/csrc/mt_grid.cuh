@@ -339,6 +339,7 @@ int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStre
 int mt_opt_coschedule();
 int mt_opt_coschedule_pct();
 int mt_opt_potrf_cluster();
+int mt_opt_tcf_cluster4();
 bool mt_tc_supported(const Grid& g);
 bool mt_tc_trsm_enabled(const Grid& g);  // off-band TRSM as a tcgen05 GEMM against L_kk^{-1}
 int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st);

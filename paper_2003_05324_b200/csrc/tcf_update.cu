@@ -99,6 +99,26 @@ __device__ __forceinline__ void ld16(uint32_t (&v)[16], uint32_t taddr) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// 2-CTA TMA multicast (cta_group::2): the box lands at the same smem offset in
+// every CTA of `mask`; each destination's bytes complete on the `full` barrier
+// of that destination's pair leader (the peer bit of the barrier address
+// cleared, as CUTLASS's SM100_TMA_2SM_LOAD_MULTICAST)
+__device__ __forceinline__ void tma_load_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 uint16_t mask, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%4, %5}], [%2], %3;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask), "r"(c0), "r"(c1)
+      : "memory");
+}
+// MMA completion arriving once on the barrier at this offset in every CTA of mask
+__device__ __forceinline__ void umma2_commit_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((uint64_t)map),
                "r"(c0), "r"(c1)
@@ -117,7 +137,11 @@ struct WorkF {
 
 enum { OUT_UPDATE = 0, OUT_PRESPLIT = 1, OUT_TRSM = 2 };
 
-template <bool TRSM>
+// CL = CTAs per cluster: 2 (one pair, 256 x 256 items) or 4 (two pairs on
+// 512 x 256 items sharing the B operand: each CTA loads its 128 rows of A and
+// multicasts half of its pair-half of B to the CTA of the same pair rank in
+// the other pair -- 24 instead of 32 KB of L2->SM operand traffic per slab)
+template <bool TRSM, int CL>
 __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
                                          const CUtensorMap& map_a, const CUtensorMap& map_b,
                                          const CUtensorMap& map_c, const CUtensorMap& map_s) {
@@ -139,7 +163,11 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // co-scheduled band update
   const uint32_t rank = cta_rank();
-  const bool leader = rank == 0;
+  const uint32_t prank = rank & 1;          // rank inside the pair
+  const uint32_t plead = rank & ~1u;        // the pair's leader (MMA issuer, TMEM owner of record)
+  const bool leader = prank == 0;           // pair leader
+  const bool qowner = rank == 0;            // owner of the cluster's work queue
+  const uint16_t pair_mask = (uint16_t)(3u << plead);
   const int nb = g.nb;
   const int nsub = w.nsubm * w.nsubn;
   auto item_ksteps = [&](int item) {
@@ -149,7 +177,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL / 2);  // one commit per pair (CL = 4: B is shared by both pairs)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -157,7 +185,8 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
     }
     for (int s = 0; s < SCHED; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 2 + 2 * EPI_WARPS);  // leader: MMA + epi + peer producer + peer epi
+      // queue owner: MMA issuers + epilogue warps of every CTA + peer producers
+      mbar_init(&sempty[s], CL / 2 + CL * EPI_WARPS + CL - 1);
     }
     for (int s = 0; s < EPI_WARPS * CSLOTS; ++s) mbar_init(&cbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -187,7 +216,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
     }
     dep = __reduce_xor_sync(0xffffffffu, dep);
     if ((threadIdx.x & 31) == 0 && dep != 0x7fffffff) {
-      if (leader) mbar_arrive_relaxed(&sempty[s]);
+      if (qowner) mbar_arrive_relaxed(&sempty[s]);
       else mbar_arrive_cl_relaxed(peer_addr(&sempty[s], 0));
     }
     return item;
@@ -196,18 +225,18 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
   if (warp == 0) {
     // ------------------------------------------------ work queue + TMA producer
     if (lane == 0) {
-      if (leader && !TRSM && g.yield) atomicAdd(w.counter + 1, 1);  // pairs started
-      const int npairs = (int)(gridDim.x / 2);
+      if (qowner && !TRSM && g.yield) atomicAdd(w.counter + 1, 1);  // clusters started
+      const int nclusters = (int)(gridDim.x / CL);
       uint32_t it = 0;
       for (uint32_t li = 0;; ++li) {
         const int s = li % SCHED;
         int item, i = 0, j = 0;
-        if (leader) {
+        if (qowner) {
           mbar_wait(&sempty[s], ((li / SCHED) & 1) ^ 1);
           if (g.failed()) {
             item = -1;
           } else if (!TRSM && g.yield && *(volatile int*)g.yield > 0 &&
-                     *(volatile int*)(w.counter + 1) < npairs && atomicSub(g.yield, 2) > 0) {
+                     *(volatile int*)(w.counter + 1) < nclusters && atomicSub(g.yield, CL) > 0) {
             item = -1;  // SM-yield request (see tc2_update.cu)
           } else {
             item = atomicAdd(w.counter, 1);
@@ -218,11 +247,15 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
             else g.off_slot_ij(w.slot0 + item / nsub, i, j);
           }
           sitem[s] = item; si[s] = i; sj[s] = j;
-          st_cl_u32(peer_addr(&sitem[s], 1), (uint32_t)item);
-          st_cl_u32(peer_addr(&si[s], 1), (uint32_t)i);
-          st_cl_u32(peer_addr(&sj[s], 1), (uint32_t)j);
+#pragma unroll
+          for (uint32_t r = 1; r < CL; ++r) {
+            st_cl_u32(peer_addr(&sitem[s], r), (uint32_t)item);
+            st_cl_u32(peer_addr(&si[s], r), (uint32_t)i);
+            st_cl_u32(peer_addr(&sj[s], r), (uint32_t)j);
+          }
           mbar_arrive(&sfull[s]);
-          mbar_arrive_cl(peer_addr(&sfull[s], 1));
+#pragma unroll
+          for (uint32_t r = 1; r < CL; ++r) mbar_arrive_cl(peer_addr(&sfull[s], r));
         } else {
           mbar_wait_cl(&sfull[s], (li / SCHED) & 1);
           item = *(volatile int*)&sitem[s];
@@ -232,10 +265,14 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
         }
         if (item < 0) break;
         const int sub = item % nsub;
-        const int m0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM;
-        const int n0 = (sub % w.nsubn) * BN + (int)rank * BNH;
+        const int m0 = (sub / w.nsubn) * (CL * BM) + (int)rank * BM;
+        // CL = 4: this CTA loads rows [pair * 64, +64) of its 128-row half of B
+        // and multicasts them to the CTA of the same pair rank in both pairs
+        const int n0 = (sub % w.nsubn) * BN + (int)prank * BNH + (CL == 4 ? (int)(rank >> 1) * 64 : 0);
         const int arow = TRSM ? (int)g.presplit_row(i) + m0 : (int)g.split_row(i, k) + m0;
         const int brow = TRSM ? (int)g.winv_row() + n0 : (int)g.split_row(j, k) + n0;
+        const uint16_t bmask = (uint16_t)(0x5u << prank);  // CTAs {prank, prank + 2}
+        const int boff = CL == 4 ? (int)(rank >> 1) * 64 * BK * 4 : 0;
         const int ksteps = item_ksteps(item);
         for (int ks = 0; ks < ksteps; ++ks, ++it) {
           const int st = it % STAGES;
@@ -243,11 +280,17 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           mbar_wait(&empty[st], ph ^ 1);
           unsigned char* sb = smem + st * STAGE_BYTES;
           if (leader) mbar_expect_tx(&full[st], 2 * STAGE_BYTES);
-          const uint32_t bar = peer_addr(&full[st], 0);
+          const uint32_t bar = peer_addr(&full[st], plead);
           tma_load_pair(sb, &map_a, bar, ks * BK, arow);                               // A hi
-          tma_load_pair(sb + A_BYTES, &map_b, bar, ks * BK, brow);                     // B hi
           tma_load_pair(sb + A_BYTES + B_BYTES, &map_a, bar, ks * BK, arow + nb);      // A lo
-          tma_load_pair(sb + 2 * A_BYTES + B_BYTES, &map_b, bar, ks * BK, brow + nb);  // B lo
+          if constexpr (CL == 4) {
+            tma_load_pair_mc(sb + A_BYTES + boff, &map_b, &full[st], bmask, ks * BK, brow);
+            tma_load_pair_mc(sb + 2 * A_BYTES + B_BYTES + boff, &map_b, &full[st], bmask, ks * BK,
+                             brow + nb);
+          } else {
+            tma_load_pair(sb + A_BYTES, &map_b, bar, ks * BK, brow);                     // B hi
+            tma_load_pair(sb + 2 * A_BYTES + B_BYTES, &map_b, bar, ks * BK, brow + nb);  // B lo
+          }
         }
       }
     }
@@ -283,8 +326,10 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
               umma(dcol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
               umma(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off), 1u);
             }
-            umma2_commit_both(&empty[s]);
-            if (c_last) umma2_commit_both(&tfull[b]);
+            // stage s is free in every CTA that received part of it: both pairs
+            // when B was multicast (each CTA's empty[s] then counts 2 commits)
+            umma2_commit_mask(&empty[s], CL == 4 ? (uint16_t)0xF : pair_mask);
+            if (c_last) umma2_commit_mask(&tfull[b], pair_mask);
           }
           __syncwarp();
           if (c_last) ++ch;
@@ -298,7 +343,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
     const int half = ew >> 2;   // column half of the item
     unsigned char* slots = epi + ew * CSLOTS * CSLOT_BYTES;
     uint64_t* wbar = cbar + ew * CSLOTS;
-    const uint32_t tempty_leader[2] = {peer_addr(&tempty[0], 0), peer_addr(&tempty[1], 0)};
+    const uint32_t tempty_l0 = peer_addr(&tempty[0], plead), tempty_l1 = peer_addr(&tempty[1], plead);
     uint32_t phb = 0;  // bit s: parity of slot s's next C load
     uint32_t ch = 0;
     auto load_c = [&](int s, int col, int row) {  // lane 0; slot s must be free
@@ -314,7 +359,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
       const int item = next_item(li, &i, &j);
       if (item < 0) break;
       const int sub = item % nsub;
-      const int row0 = (sub / w.nsubn) * (2 * BM) + (int)rank * BM + q * 32;  // row in the tile
+      const int row0 = (sub / w.nsubn) * (CL * BM) + (int)rank * BM + q * 32;  // row in the tile
       const int n0 = (sub % w.nsubn) * BN + half * COLS_W;                    // first column
       const int out = TRSM ? OUT_TRSM : ((w.presplit && j == k + 1) ? OUT_PRESPLIT : OUT_UPDATE);
       // TMA rows: output tile (i, j) (TRSM: j == k) in the off-band pool, and
@@ -341,7 +386,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
-        if (lane == 0) mbar_arrive_cl_relaxed(tempty_leader[b]);
+        if (lane == 0) mbar_arrive_cl_relaxed(b ? tempty_l1 : tempty_l0);
         ++ch;
         if (c == 0 && out != OUT_TRSM && lane == 0) {
           // C of this item: slots free once the previous item's stores were read
@@ -452,20 +497,46 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
   }
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+template <int CL>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     tcf_update_kernel(Grid g, int k, WorkF w, const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b,
                       const __grid_constant__ CUtensorMap map_c,
                       const __grid_constant__ CUtensorMap map_s) {
-  tcf_body<false>(g, k, w, map_a, map_b, map_c, map_s);
+  tcf_body<false, CL>(g, k, w, map_a, map_b, map_c, map_s);
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+template <int CL>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     tcf_trsm_kernel(Grid g, int k, WorkF w, const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c,
                     const __grid_constant__ CUtensorMap map_s) {
-  tcf_body<true>(g, k, w, map_a, map_b, map_c, map_s);
+  tcf_body<true, CL>(g, k, w, map_a, map_b, map_c, map_s);
+}
+
+template <int CL>
+int launch_tcf(bool trsm, int clusters, cudaStream_t st, const Grid& g, int k, const WorkF& w,
+               const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+               const CUtensorMap& ms) {
+  auto kern = trsm ? tcf_trsm_kernel<CL> : tcf_update_kernel<CL>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL * clusters);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (mt_cuda_check(cudaLaunchKernelEx(&cfg, kern, g, k, w, ma, mb, mc, ms),
+                    trsm ? "tcf_trsm_kernel" : "tcf_update_kernel"))
+    return MT_E_CUDA;
+  return MT_OK;
 }
 
 int g_smf = 0;
@@ -477,10 +548,13 @@ int g_smf = 0;
 int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool trsm, int presplit,
                   cudaStream_t st, unsigned long long* span, int jlo, int jhi) {
   if (scnt <= 0) return MT_OK;
+  // 4-CTA clusters (two pairs sharing B by multicast) need 512-row items
+  const int CL = (mt_opt_tcf_cluster4() && g.nb % (4 * BM) == 0) ? 4 : 2;
   CUtensorMap ma, mb, mc, ms;
   const int64_t split_rows = g.split_rows();
   int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
-  if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, BNH, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, CL == 4 ? BNH / 2 : BNH,
+                            CU_TENSOR_MAP_SWIZZLE_64B);
   const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;
   if (!rc) rc = make_map_2d(&mc, g.sp ? (const void*)g.sp : (const void*)g.split, c_rows, g.nb, 4, 32,
                             32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -488,7 +562,7 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   if (rc) return rc;
   WorkF w;
   w.slot0 = s0;
-  w.nsubm = g.nb / (2 * BM);
+  w.nsubm = g.nb / (CL * BM);
   w.nsubn = g.nb / BN;
   w.nitems = (int)(scnt * w.nsubm * w.nsubn);
   w.presplit = presplit;
@@ -507,18 +581,10 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   w.counter = counters[dev] + 2 * (next_counter[dev]++ % 256);
   if (mt_cuda_check(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int), st), "counter reset"))
     return MT_E_CUDA;
-  int pairs = (ctas > 0 ? ctas : g_smf) / 2;
-  if (!trsm && g.yield && ctas <= 0) pairs = g_smf;  // oversubscribed: refills yielded SMs
-  if (pairs > w.nitems) pairs = w.nitems;
-  if (pairs < 1) pairs = 1;
-  if (trsm) {
-    cudaFuncSetAttribute(tcf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    tcf_trsm_kernel<<<2 * pairs, NUM_THREADS, SMEM_BYTES, st>>>(g, k, w, ma, mb, mc, ms);
-    MT_LAUNCH_CHECK("tcf_trsm_kernel");
-  } else {
-    cudaFuncSetAttribute(tcf_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    tcf_update_kernel<<<2 * pairs, NUM_THREADS, SMEM_BYTES, st>>>(g, k, w, ma, mb, mc, ms);
-    MT_LAUNCH_CHECK("tcf_update_kernel");
-  }
-  return MT_OK;
+  int clusters = (ctas > 0 ? ctas : g_smf) / CL;
+  if (!trsm && g.yield && ctas <= 0) clusters = 2 * g_smf / CL;  // oversubscribed: refills yielded SMs
+  if (clusters > w.nitems) clusters = w.nitems;
+  if (clusters < 1) clusters = 1;
+  return CL == 4 ? launch_tcf<4>(trsm, clusters, st, g, k, w, ma, mb, mc, ms)
+                 : launch_tcf<2>(trsm, clusters, st, g, k, w, ma, mb, mc, ms);
 }

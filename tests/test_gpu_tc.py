@@ -278,3 +278,32 @@ def test_wide_pair_items_bitwise(rz_engine, n, t, co):
         lib.mt_set_option(10, oc)
     for key in facs[0].tiles:
         assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
+
+
+@pytest.mark.parametrize("n,t,co", [(8192, 3, 1), (7000, 2, 0), (12288, 8, 1)])
+def test_tcf_four_cta_clusters_bitwise(gpu, n, t, co):
+    """Option 15: the round-to-nearest engine on 4-CTA clusters (two CTA pairs
+    on 512 x 256 items, the B operand multicast across the pairs) applies the
+    same MMA / flush / FADD sequence per output element as the 2-CTA kernel:
+    bitwise equal factors (bulk, panel-column update and TRSM), with and
+    without co-scheduling, ragged last tile included."""
+    mt = _mt()
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    locs = mt.generate_locations(n, seed=37)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    pol = mt.PrecisionPolicy.mp(diag_thick=t)
+    facs = []
+    oc = lib.mt_set_option(10, co)
+    try:
+        for c4 in (0, 1):
+            old = lib.mt_set_option(15, c4)
+            try:
+                facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5),
+                                                               512, pol), lookahead=1))
+            finally:
+                lib.mt_set_option(15, old)
+    finally:
+        lib.mt_set_option(10, oc)
+    for key in facs[0].tiles:
+        assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
