@@ -375,6 +375,12 @@ def run_ours(args, rank, world, local_rank):
     n, nb, t = args.n, args.nb, args.t
     engine = args.engine
     mt.set_fp32_engine(engine)
+    opts = {}
+    if os.environ.get("MT_OPTS"):  # A/B of library options, e.g. MT_OPTS=15=1 (reported)
+        for kv in os.environ["MT_OPTS"].split(","):
+            k_, v_ = kv.split("=")
+            lib.mt_set_option(int(k_), int(v_))
+            opts[int(k_)] = int(v_)
     ds = _dataset(mt, n)  # same dataset on every rank (one distributed evaluation)
     theta = mt.MaternParams(*THETA)
     mp_pol = mt.PrecisionPolicy.mp(diag_thick=t)
@@ -596,6 +602,7 @@ def run_ours(args, rank, world, local_rank):
             "kernel_event_spans_ms_per_step": {k: round(v["ms"], 3) for k, v in kinds.items()},
             "mp_vs_dp": dp, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "clocks": clocks.summary(),
+            "library_options": opts or "defaults", "fp32_engine": engine,
             "nccl": ({"version": ".".join(map(str, torch.cuda.nccl.version())),
                       "world_size": world, "backend": dist.get_backend(),
                       "init_lines": nccl_summary()} if dist_on else None),

@@ -172,7 +172,7 @@ struct Grid {
   // slot -> (i, j) inversion by binary search over the owned column starts
   // (a column without owned rows shares its start with the next column, so
   // the largest index with start <= s is a column that holds slot s)
-  __device__ __forceinline__ void band_slot_ij(int64_t s, int& i, int& j) const {
+  MT_HD void band_slot_ij(int64_t s, int& i, int& j) const {
     int lo = 0, hi = owned_cols();  // largest owned index m with bcol(col m) <= s
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
@@ -181,7 +181,7 @@ struct Grid {
     j = owned_col(lo);
     i = first_row(j) + (int)(s - bcol(j)) * rs;
   }
-  __device__ __forceinline__ void off_slot_ij(int64_t s, int& i, int& j) const {
+  MT_HD void off_slot_ij(int64_t s, int& i, int& j) const {
     int lo = 0, hi = owned_before(p - t);
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;

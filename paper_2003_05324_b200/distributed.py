@@ -202,7 +202,15 @@ class DistributedEvaluator:
         L, rq, pring = ring_geometry(p, self.P, self.Q)
         base = (k & 1) * pring
         hs = []
+        row_done = False
         for stage, grp, root, b, m0, m1, mb1 in panel_bcast_plan(k, p, self.P, self.Q, t):
+            if stage == "col" and not row_done:
+                # a column-stage root forwards rows it received in the row stage:
+                # collectives of different communicators are not ordered with
+                # each other, so the current stream waits for the row stage here
+                for h in hs:
+                    h.wait()
+                row_done = True
             if stage == "row":
                 if grp != self.pr:
                     continue

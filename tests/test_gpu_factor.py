@@ -297,8 +297,13 @@ def test_cluster_potrf_bitwise_equals_single_cta(gpu, n, nb, pol):
         try:
             facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), nb,
                                                            policy)))
+        except mt.FactorizationError as exc:  # DST can be indefinite: same pivot on both
+            facs.append(exc.index)
         finally:
             lib.mt_set_option(14, old)
+    if not hasattr(facs[0], "tiles"):
+        assert facs[0] == facs[1]
+        return
     for key in facs[0].tiles:
         a, b = facs[0].tiles[key], facs[1].tiles[key]
         assert np.array_equal(a.dp, b.dp), key
