@@ -233,6 +233,11 @@ int64_t mt_split_tiles_ex(int32_t p, int32_t t, int32_t mode, int32_t row_stride
 /* Ring position of tile row i on a P x Q grid (see mt_tiles.row_stride). */
 int32_t mt_ring_pos(int32_t p, int32_t row_stride, int32_t col_stride, int32_t i);
 
+/* Diagnostics (option 16 = 1): {MMA-issuer cycles waiting for operands, for a
+ * drained TMEM chunk, total issuer cycles, issuers} of the FP32 tcgen05 update
+ * since the last call (then reset). */
+int mt_tcf_stats(double* out4);
+
 /* Synchronise `stream` and read status: *bad_pivot (-1 none), *overflow,
  * *duplicates.  Returns MT_E_NOT_SPD / MT_E_OVERFLOW when set, else MT_OK. */
 int mt_read_status(const mt_tiles* g, int64_t* bad_pivot, int64_t* overflow,

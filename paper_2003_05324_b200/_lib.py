@@ -99,6 +99,7 @@ SIGNATURES = {
     "mt_logdet_partials": (ctypes.c_int, [_P(MtTiles), _V, _V]),
     "mt_fwd_step": (ctypes.c_int, [_P(MtTiles), _I32, _V, _V]),
     "mt_fwd_step_ex": (ctypes.c_int, [_P(MtTiles), _I32, _I32, _V, _V]),
+    "mt_tcf_stats": (ctypes.c_int, [_P(ctypes.c_double)]),
     "mt_sumsq": (ctypes.c_int, [_V, _I64, _V, _V, _V]),
     "mt_local_tiles": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _P(_I64), _P(_I64)]),
     "mt_dpanel_tiles": (_I64, [_I32, _I32, _I32]),

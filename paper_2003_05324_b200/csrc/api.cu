@@ -249,6 +249,7 @@ static int g_wide_l2pf = 0;    // 1 = the 256 x 512 update stages each warp's C 
 static int g_cta_pairs = 1;    // 1 = FP32 update/TRSM on CTA pairs (tcgen05 cta_group::2)
 static int g_tc_diag = 0;      // diagnostics (wrong results): 1 no C loads, 2 no C stores, 4 no epilogue
 static int g_c_prefetch = 0;   // 1 = FP32 update stages each item's C block in L2 (cp.async.bulk.prefetch)
+static int g_tcf_stats = 0;     // 1 = tcf kernels accumulate MMA-issuer wait cycles (diagnostics)
 static int g_tcf_cluster4 = 0;  // 1 = RN tcgen05 update on 4-CTA clusters (B multicast across two pairs)
 static int g_potrf_cluster = 0;  // 1 = POTRF on a cluster of nb/32 CTAs (tile in distributed smem; opt-in)
 int mt_opt_engine() { return g_engine; }
@@ -267,6 +268,7 @@ int mt_opt_coschedule() { return g_coschedule; }
 int mt_opt_coschedule_pct() { return g_cosched_pct; }
 int mt_opt_potrf_cluster() { return g_potrf_cluster; }
 int mt_opt_tcf_cluster4() { return g_tcf_cluster4; }
+int mt_opt_tcf_stats() { return g_tcf_stats; }
 
 extern "C" {
 
@@ -305,6 +307,7 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 13) { old = g_wide_l2pf; g_wide_l2pf = value; }
   else if (option == 14) { old = g_potrf_cluster; g_potrf_cluster = value; }
   else if (option == 15) { old = g_tcf_cluster4; g_tcf_cluster4 = value; }
+  else if (option == 16) { old = g_tcf_stats; g_tcf_stats = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

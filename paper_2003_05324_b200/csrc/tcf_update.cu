@@ -133,9 +133,15 @@ struct WorkF {
   int presplit;  // the column-(k+1) update also writes its outputs' TF32 split
   unsigned long long* span;
   int mlo, mhi, sw;  // update: owned column range, super-column width (0 = slot order)
+  int stats;         // option 16: accumulate MMA-issuer wait cycles
 };
 
 enum { OUT_UPDATE = 0, OUT_PRESPLIT = 1, OUT_TRSM = 2 };
+
+// diagnostics (option 16): MMA-issuer cycles spent waiting for operands
+// (full), for a drained TMEM chunk buffer (tempty) and in total, summed over
+// the pair leaders of every launch since the last mt_tcf_stats() read
+__device__ unsigned long long g_tcf_stats[4];
 
 // CL = CTAs per cluster: 2 (one pair, 256 x 256 items) or 4 (two pairs on
 // 512 x 256 items sharing the B operand: each CTA loads its 128 rows of A and
@@ -298,6 +304,9 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
     // ------------------------------------------------ MMA issuer (leader only)
     if (leader) {
       uint32_t it = 0, ch = 0;
+      const bool stats = w.stats;
+      unsigned long long w_full = 0, w_tempty = 0;
+      const unsigned long long t_start = stats ? clock64() : 0;
       for (uint32_t li = 0;; ++li) {
         const int item = next_item(li, nullptr, nullptr);
         if (item < 0) break;
@@ -306,11 +315,15 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           const uint32_t b = ch & 1;
           const bool c_first = (ks % KC) == 0, c_last = (ks % KC) == KC - 1;
           if (c_first) {
+            const unsigned long long t0 = stats ? clock64() : 0;
             mbar_wait_cl(&tempty[b], ((ch >> 1) & 1) ^ 1);  // chunk buffer drained
+            if (stats) w_tempty += clock64() - t0;
             asm volatile("tcgen05.fence::after_thread_sync;");
           }
           const int s = it % STAGES;
+          const unsigned long long t1 = stats ? clock64() : 0;
           mbar_wait(&full[s], (it / STAGES) & 1);
+          if (stats) w_full += clock64() - t1;
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (lane == 0) {
             unsigned char* st = smem + s * STAGE_BYTES;
@@ -334,6 +347,12 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           __syncwarp();
           if (c_last) ++ch;
         }
+      }
+      if (stats && lane == 0) {
+        atomicAdd(&g_tcf_stats[0], w_full);
+        atomicAdd(&g_tcf_stats[1], w_tempty);
+        atomicAdd(&g_tcf_stats[2], clock64() - t_start);
+        atomicAdd(&g_tcf_stats[3], 1ull);
       }
     }
   } else {
@@ -570,6 +589,7 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   w.mlo = g.owned_before(jlo);
   w.mhi = g.owned_before(jhi);
   w.sw = (!trsm && jhi > jlo + 1 && g.rs == 1) ? mt_opt_super_cols() : 0;
+  w.stats = mt_opt_tcf_stats();
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_smf) cudaDeviceGetAttribute(&g_smf, cudaDevAttrMultiProcessorCount, dev);
@@ -587,4 +607,14 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   if (clusters < 1) clusters = 1;
   return CL == 4 ? launch_tcf<4>(trsm, clusters, st, g, k, w, ma, mb, mc, ms)
                  : launch_tcf<2>(trsm, clusters, st, g, k, w, ma, mb, mc, ms);
+}
+
+// option-16 diagnostics: {cycles waiting for operands, for TMEM, total, issuers}
+extern "C" int mt_tcf_stats(double* out4) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (mt_cuda_check(cudaMemcpyFromSymbol(h, g_tcf_stats, sizeof(h)), "tcf stats")) return MT_E_CUDA;
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  if (mt_cuda_check(cudaMemcpyToSymbol(g_tcf_stats, z, sizeof(z)), "tcf stats reset")) return MT_E_CUDA;
+  for (int q = 0; q < 4; ++q) out4[q] = (double)h[q];
+  return MT_OK;
 }
