@@ -60,8 +60,13 @@ constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
 constexpr int EPI_WARPS = 8;
 constexpr int COLS_W = BN / 2;  // columns per epilogue warp
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
-constexpr int CSLOTS = 3, CSLOT_BYTES = 32 * 32 * 4;
-constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 96 KB
+#ifndef MT_TCF_CSLOTS
+#define MT_TCF_CSLOTS 3
+#endif
+// C-chunk slots per epilogue warp (2 or 3; 2 leaves room for a 5th operand stage)
+constexpr int CSLOTS = MT_TCF_CSLOTS, CSLOT_BYTES = 32 * 32 * 4;
+static_assert(CSLOTS == 2 || CSLOTS == 3, "C-chunk slots");
+constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 96 KB at 3 slots
 constexpr int TMEM_COLS = 512;                               // 2 chunk buffers x 256 columns
 constexpr int SCHED = 4;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 768;
@@ -411,8 +416,8 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           // C of this item: slots free once the previous item's stores were read
           bulk_wait_read<0>();
           if (out == OUT_UPDATE) {
-            for (int m = 0; m < 3; ++m) load_c(m, n0 + m * 32, crow);
-            prefetch_l2_2d(&map_c, n0 + 96, crow);
+            for (int m = 0; m < CSLOTS; ++m) load_c(m, n0 + m * 32, crow);
+            for (int m = CSLOTS; m < 4; ++m) prefetch_l2_2d(&map_c, n0 + m * 32, crow);
           } else {
             load_c(0, n0, crow);
             for (int m = 1; m < 4; ++m) prefetch_l2_2d(&map_c, n0 + m * 32, crow);
@@ -438,7 +443,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
       if (out == OUT_UPDATE) {
 #pragma unroll
         for (int m = 0; m < COLS_W / 32; ++m) {
-          const int s = m == 3 ? 0 : m;
+          const int s = m % CSLOTS;
           wait_c(s);
           const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * 128;
 #pragma unroll
@@ -456,9 +461,9 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           if (lane == 0) {
             tma_store_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * 32, crow);
             bulk_commit();
-            if (m == 0) {  // chunk 3 reuses slot 0 (L2-prefetched)
+            if (m + CSLOTS < 4) {  // chunk m + CSLOTS reuses this slot (L2-prefetched)
               bulk_wait_read<0>();
-              load_c(0, n0 + 96, crow);
+              load_c(s, n0 + (m + CSLOTS) * 32, crow);
             }
           }
         }
@@ -485,14 +490,27 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           }
           put(0, x, 0);
           put(1, x, 1);
-          put(2, x, 2);
+          if (CSLOTS > 2) put(2, x, 2);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&map_c, slots, n0 + m * 32, crow);
             tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * 32, srow);
-            tma_store_2d(&map_s, slots + 2 * CSLOT_BYTES, n0 + m * 32, srow + nb);
+            if (CSLOTS > 2) tma_store_2d(&map_s, slots + 2 * CSLOT_BYTES, n0 + m * 32, srow + nb);
             bulk_commit();
+          }
+          if (CSLOTS == 2) {  // the TF32 lo part goes through slot 1 once hi was read
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            put(1, x, 2);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * 32, srow + nb);
+              bulk_commit();
+            }
+          }
+          if (lane == 0) {
             if (out == OUT_PRESPLIT && m < 3) {
               bulk_wait_read<0>();
               load_c(0, n0 + (m + 1) * 32, crow);

@@ -52,7 +52,18 @@ def test_loglik_parity_with_reference(gpu, name):
         is_dp = tag == "dp" or int(tag.split(":")[1]) >= -(-len(g["z"]) // nb)
         tol = DP_TOL if is_dp else MP_TOL
         if name == "strong1024" and not is_dp:
-            tol = 2e-4  # ill-conditioned field: MP-vs-MP drift is amplified
+            # ill-conditioned field (beta=0.3, nu=1): two FP32 factorizations
+            # differ by up to the method's own MP error.  Measured on B200:
+            # GPU-MP vs CPU-MP 2.0e-6 / 7.7e-6 / 1.9e-5 at t=1/2/4; distance
+            # from DP GPU 6.2e-6 / 1.8e-5 / 2.1e-7 vs the reference's 4.2e-6 /
+            # 2.6e-5 / 1.9e-5.  Bound: the north-star 1e-5, or no further from
+            # DP than the reference's MP (1.5x rounding-noise margin)
+            dp = g["results"]["dp"][0]
+            gpu_gap = abs(ev.value - dp) / abs(dp)
+            cpu_gap = abs(want[0] - dp) / abs(dp)
+            assert rel <= MP_TOL or gpu_gap <= 1.5 * cpu_gap, (tag, rel, gpu_gap, cpu_gap)
+            assert rel <= 2.0 * cpu_gap + MP_TOL, (tag, rel, cpu_gap)
+            continue
         assert rel <= tol, (name, tag, ev.value, want[0], rel)
         assert math.isclose(ev.logdet, want[1], rel_tol=max(tol, 1e-10))
 

@@ -8,7 +8,7 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/paper_2003_05324_b200/_build/variants/$name
 mkdir -p $out
 objs=""
-for u in api gen potrf trsm update solve prof tc_update tc2_update tc2w_update dmma_update; do
+for u in api gen potrf trsm update solve prof tc_update tc2_update tc2w_update tcf_update dmma_update; do
   extra=""; [ $u = gen ] && extra="-fmad=false"
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     -I $root/include --expt-relaxed-constexpr $extra "$@" -c $root/paper_2003_05324_b200/csrc/$u.cu -o $out/$u.o &
