@@ -88,6 +88,9 @@ typedef struct mt_tiles {
   double* dpanel;
   int32_t row_stride;
   int32_t row_offset;
+  /* panels in flight in the scratch / split / dpanel rings: 0 or 2 (lookahead
+   * 1), 3 (lookahead 2); sizes from mt_ring_tiles() */
+  int32_t panel_slots;
 } mt_tiles;
 
 /* Matern parameters + per-theta Bessel constants (covmath.py:72-95, 228-283),
@@ -230,6 +233,12 @@ int mt_local_tiles_ex(int32_t p, int32_t t, int32_t mode, int32_t row_stride, in
 int64_t mt_dpanel_tiles_ex(int32_t p, int32_t row_stride, int32_t col_stride);
 int64_t mt_split_tiles_ex(int32_t p, int32_t t, int32_t mode, int32_t row_stride,
                           int32_t col_stride);
+/* Ring-buffer sizes (tiles) for `slots` panels in flight (2: lookahead 1,
+ * 3: lookahead 2) on a P x Q grid: scratch (FP32 tiles), split (FP32 tiles,
+ * 0 when the layout has no FP32 operands), dpanel (FP64 tiles, multi-GPU). */
+int mt_ring_tiles(int32_t p, int32_t t, int32_t mode, int32_t nb, int32_t row_stride,
+                  int32_t col_stride, int32_t slots, int64_t* scratch, int64_t* split,
+                  int64_t* dpanel);
 /* Ring position of tile row i on a P x Q grid (see mt_tiles.row_stride). */
 int32_t mt_ring_pos(int32_t p, int32_t row_stride, int32_t col_stride, int32_t i);
 

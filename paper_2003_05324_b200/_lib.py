@@ -36,6 +36,7 @@ class MtTiles(ctypes.Structure):
         ("dpanel", ctypes.c_void_p),
         ("row_stride", ctypes.c_int32),
         ("row_offset", ctypes.c_int32),
+        ("panel_slots", ctypes.c_int32),
     ]
 
 
@@ -108,6 +109,8 @@ SIGNATURES = {
     "mt_dpanel_tiles_ex": (_I64, [_I32, _I32, _I32]),
     "mt_split_tiles_ex": (_I64, [_I32, _I32, _I32, _I32, _I32]),
     "mt_ring_pos": (_I32, [_I32, _I32, _I32, _I32]),
+    "mt_ring_tiles": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _I32, _P(_I64), _P(_I64),
+                                     _P(_I64)]),
     "mt_launch_count": (ctypes.c_longlong, []),
     "mt_prof_begin": (ctypes.c_int, [_I32]),
     "mt_prof_end": (ctypes.c_int, [_I32, _V, _V, _V, _V]),

@@ -173,6 +173,57 @@ static int cholesky_schedule(const Grid& g, int lookahead, cudaStream_t main,
     }
     return MT_OK;
   };
+  if (lookahead >= 2 && p >= 4) {
+    if (g.nring < 3) {
+      mt_set_error("lookahead 2 needs a layout with 3 panel slots (mt_tiles.panel_slots)");
+      return MT_E_BAD_ARG;
+    }
+    // Lookahead depth 2: the panel stream keeps panels k+1 and k+2 ready while
+    // the caller stream applies step k to columns k+3 ..; column j receives
+    // steps j-2 and j-1 on the panel stream, the earlier ones from the bulk
+    // updates.  Every tile still gets its updates in ascending k from the same
+    // kernels, so the factor is bitwise identical to lookahead 0 / 1.
+    std::vector<cudaEvent_t> panel_ev(p), step_ev(p);
+    cudaEvent_t e0 = ctx->event();
+    CK(cudaEventRecord(e0, main), "event record");
+    CK(cudaStreamWaitEvent(pan, e0, 0), "stream wait");
+    for (int j = 0; j < 2; ++j) {  // panels 0 and 1
+      if (j == 1) RC(mt_update_impl(g, 0, 1, 2, pan));
+      RC(mt_potrf_impl(g, j, narrow_k(j), pan));
+      RC(mt_trsm_impl(g, j, pan));
+      RC(fwd_step(j, pan));
+      panel_ev[j] = ctx->event();
+      CK(cudaEventRecord(panel_ev[j], pan), "event record");
+    }
+    for (int k = 0; k < p - 1; ++k) {
+      const int j = k + 2;  // the panel the panel stream forms meanwhile
+      if (j < p) {
+        // column j got steps <= k-1 from the bulk updates; the ring slot of
+        // panel j is panel k-1's, free once bulk(k-1) finished
+        if (k >= 1) CK(cudaStreamWaitEvent(pan, step_ev[k - 1], 0), "stream wait");
+        RC(mt_update_impl(g, k, j, j + 1, pan));
+        RC(mt_update_impl(g, k + 1, j, j + 1, pan));
+        RC(request(1u));
+        RC(mt_potrf_impl(g, j, narrow_k(j), pan));
+        if (j + 1 < p) {
+          const std::function<int()> ask = [&]() { return request((unsigned)ysms); };
+          RC(mt_trsm_impl(g, j, pan, yield_on ? &ask : nullptr));
+        }
+        RC(request(0u));
+        RC(fwd_step(j, pan));
+        panel_ev[j] = ctx->event();
+        CK(cudaEventRecord(panel_ev[j], pan), "event record");
+      }
+      CK(cudaStreamWaitEvent(main, panel_ev[k], 0), "stream wait");
+      if (k + 3 < p) RC(mt_update_impl(gb, k, k + 3, p, main));
+      step_ev[k] = ctx->event();
+      CK(cudaEventRecord(step_ev[k], main), "event record");
+    }
+    cudaEvent_t ef = ctx->event();
+    CK(cudaEventRecord(ef, pan), "event record");
+    CK(cudaStreamWaitEvent(main, ef, 0), "stream wait");
+    return MT_OK;
+  }
   cudaEvent_t e = ctx->event();
   CK(cudaEventRecord(e, main), "event record");
   CK(cudaStreamWaitEvent(pan, e, 0), "stream wait");
@@ -588,6 +639,20 @@ int64_t mt_split_tiles_ex(int32_t p, int32_t t_, int32_t mode, int32_t row_strid
   g.rs = row_stride > 0 ? row_stride : 1;
   g.cs = col_stride > 0 ? col_stride : 1;
   return 4 * (int64_t)g.pring() + 2 * (int64_t)p + 2;
+}
+
+int mt_ring_tiles(int32_t p, int32_t t_, int32_t mode, int32_t nb, int32_t row_stride,
+                  int32_t col_stride, int32_t slots, int64_t* scratch, int64_t* split,
+                  int64_t* dpanel) {
+  Grid g{};
+  g.p = p; g.t = mode == MT_MODE_DP ? p : t_; g.mode = mode; g.nb = nb;
+  g.rs = row_stride > 0 ? row_stride : 1;
+  g.cs = col_stride > 0 ? col_stride : 1;
+  g.nring = slots > 2 ? slots : 2;
+  if (scratch) *scratch = (int64_t)g.nring * g.slot_tiles();
+  if (split) *split = (mode == MT_MODE_MP && g.t < p) ? g.split_rows() / nb : 0;
+  if (dpanel) *dpanel = (int64_t)g.nring * g.pring();
+  return MT_OK;
 }
 
 int32_t mt_ring_pos(int32_t p, int32_t row_stride, int32_t col_stride, int32_t i) {

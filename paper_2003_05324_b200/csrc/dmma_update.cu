@@ -268,10 +268,10 @@ int mt_dmma_update_impl(const Grid& g, int k, int64_t b0, int64_t bcnt, cudaStre
   const int64_t sp_rows = g.sp ? g.noff() * nb : nb;
   if (!rc) rc = make_map_2d(&maps.sp, sp, sp_rows, nb, 4, BK, 64, CU_TENSOR_MAP_SWIZZLE_64B);
   const void* spl = g.split ? (const void*)g.split : (const void*)g.dp;
-  const int64_t spl_rows = g.split ? (int64_t)4 * g.pring() * nb : nb;
+  const int64_t spl_rows = g.split ? g.ring_rows() * nb : nb;
   if (!rc) rc = make_map_2d(&maps.split, spl, spl_rows, nb, 4, BK, 64, CU_TENSOR_MAP_SWIZZLE_64B);
   const void* dpn = g.dpanel ? (const void*)g.dpanel : (const void*)g.dp;
-  const int64_t dpn_rows = g.dpanel ? (int64_t)2 * g.pring() * nb : nb;
+  const int64_t dpn_rows = g.dpanel ? (int64_t)g.nring * g.pring() * nb : nb;
   if (!rc) rc = make_map_2d(&maps.dpanel, dpn, dpn_rows, nb, 8, BK, 64, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   const int nsm = nb / BM, nsn = nb / BN;

@@ -45,7 +45,10 @@ struct Grid {
   // cs = Q (single GPU: rs = cs = 1, r0 = c0 = 0)
   int cs = 1, c0 = 0;
   int rs = 1, r0 = 0;
-  double* dpanel = nullptr;  // multi-GPU: FP64 rows of the two panels in flight (ring)
+  double* dpanel = nullptr;  // multi-GPU: FP64 rows of the panels in flight (ring)
+  // panels in flight in the rings (scratch, split, dpanel): 2 for lookahead 1,
+  // 3 for lookahead 2 (panel k is read by the bulk update while k+1 and k+2 form)
+  int nring = 2;
   // bulk FP32 update only: SM-yield request word written by the panel stream
   // (cuStreamWriteValue32); CTAs that consume a request exit between work items
   int* yield = nullptr;
@@ -117,10 +120,10 @@ struct Grid {
   }
   // multi-GPU panel ring: FP64 rows of panel k (band rows in MP; all in DP)
   MT_HD double* dpanel_tile(int i, int k) const {
-    return dpanel + ((int64_t)(k & 1) * pring() + ring_pos(i)) * tile_elems();
+    return dpanel + ((int64_t)(k % nring) * pring() + ring_pos(i)) * tile_elems();
   }
   MT_HD int64_t dpanel_row(int i, int k) const {
-    return ((int64_t)(k & 1) * pring() + ring_pos(i)) * nb;
+    return ((int64_t)(k % nring) * pring() + ring_pos(i)) * nb;
   }
   // L_kk for the panel solves: the pool tile on its owner, else the copy
   // broadcast into the FP64 panel ring (row k of panel k)
@@ -141,7 +144,7 @@ struct Grid {
     return (fl + tile_elems() - 1) / tile_elems();
   }
   MT_HD int64_t slot_tiles() const { return (has_mirrors() ? t : 0) + inv_tiles(); }
-  MT_HD float* sslot(int k) const { return scratch + (int64_t)(k & 1) * slot_tiles() * tile_elems(); }
+  MT_HD float* sslot(int k) const { return scratch + (int64_t)(k % nring) * slot_tiles() * tile_elems(); }
   MT_HD float* sdiag(int k) const { return sslot(k); }
   MT_HD double* sinv64(int k) const {
     return (double*)(sslot(k) + (has_mirrors() ? (int64_t)t : 0) * tile_elems());
@@ -150,16 +153,17 @@ struct Grid {
   // TF32 hi/lo split of FP32 operand (i, k) of panel k (tensor-core engine),
   // ring of two panels in ring order: rows of [hi | lo] per tile row
   MT_HD int64_t split_row(int i, int k) const {
-    return ((int64_t)(k & 1) * pring() + ring_pos(i)) * 2 * nb;
+    return ((int64_t)(k % nring) * pring() + ring_pos(i)) * 2 * nb;
   }
   MT_HD float* split_hi(int i, int k) const { return split + split_row(i, k) * nb; }
   MT_HD float* split_lo(int i, int k) const { return split_hi(i, k) + tile_elems(); }
   // split buffer tail (tensor-core TRSM): the pre-TRSM split of the next
   // panel's off-band tiles (written by the update epilogue into column k+1)
   // and the split of W = L_kk^{-1} (row-major), one slot each
-  MT_HD int64_t presplit_row(int i) const { return ((int64_t)4 * pring() + 2 * i) * nb; }
-  MT_HD int64_t winv_row() const { return ((int64_t)4 * pring() + 2 * p) * nb; }
-  MT_HD int64_t split_rows() const { return ((int64_t)4 * pring() + 2 * p + 2) * nb; }
+  MT_HD int64_t ring_rows() const { return (int64_t)2 * nring * pring(); }  // tile rows
+  MT_HD int64_t presplit_row(int i) const { return (ring_rows() + 2 * i) * nb; }
+  MT_HD int64_t winv_row() const { return (ring_rows() + 2 * p) * nb; }
+  MT_HD int64_t split_rows() const { return (ring_rows() + 2 * p + 2) * nb; }
   MT_HD float* presplit_hi(int i) const { return split + presplit_row(i) * nb; }
   MT_HD float* winv_hi() const { return split + winv_row() * nb; }
   MT_HD float* winv_lo() const { return winv_hi() + tile_elems(); }
@@ -254,6 +258,7 @@ inline Grid make_grid(const mt_tiles* g) {
   r.c0 = g->col_offset;
   r.rs = g->row_stride > 0 ? g->row_stride : 1;
   r.r0 = g->row_offset;
+  r.nring = g->panel_slots > 2 ? g->panel_slots : 2;
   r.dpanel = g->dpanel;
   return r;
 }

@@ -130,6 +130,10 @@ class CholeskyFactor:
 def cholesky(matrix, threads=1, lookahead=1):
     """Factor an assembled TileMatrix in place on the GPU (factor.py:230-285).
 
+    lookahead: panels formed ahead of the bulk update on the panel stream
+    (0, 1 or 2; 2 needs a TileMatrix(..., panel_slots=3)); results are
+    bitwise identical for every value.
+
     Raises FactorizationError(global pivot) when not positive definite.
     """
     del threads  # schedule-invariant; accepted for signature compatibility
@@ -138,7 +142,7 @@ def cholesky(matrix, threads=1, lookahead=1):
     if matrix.factored:
         raise ValueError("matrix is already factored")
     lib = _lib.load()
-    _lib.check(lib.mt_cholesky(ctypes.byref(matrix.desc), int(bool(lookahead)),
+    _lib.check(lib.mt_cholesky(ctypes.byref(matrix.desc), int(lookahead),
                                _lib.stream_handle()), "mt_cholesky")
     matrix._touch()
     bad, _, _ = matrix.read_status()

@@ -149,7 +149,7 @@ class TileMatrix:
     """
 
     def __init__(self, n, nb, policy, device=None, col_stride=1, col_offset=0, row_stride=1,
-                 row_offset=0):
+                 row_offset=0, panel_slots=2):
         if n < 1:
             raise ValueError(f"need n >= 1, got {n}")
         if nb < 1:
@@ -176,18 +176,20 @@ class TileMatrix:
         lib.mt_local_tiles_ex(self.p, t, mode, self.row_stride, self.row_offset, self.col_stride,
                               self.col_offset, ctypes.byref(ndp), ctypes.byref(nsp))
         ndp, nsp = ndp.value, nsp.value
-        nsc = lib.mt_scratch_tiles(self.p, t, mode, self.nb)
-        nsl = (lib.mt_split_tiles_ex(self.p, t, mode, self.row_stride, self.col_stride)
-               if self.nb % 256 == 0 else 0)
+        # rings of panels in flight: 2 slots (lookahead 1) or 3 (lookahead 2)
+        self.panel_slots = max(2, int(panel_slots))
+        nsc, nsl, ndpn = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        lib.mt_ring_tiles(self.p, t, mode, self.nb, self.row_stride, self.col_stride,
+                          self.panel_slots, ctypes.byref(nsc), ctypes.byref(nsl), ctypes.byref(ndpn))
+        nsc, ndpn = nsc.value, ndpn.value
+        nsl = nsl.value if self.nb % 256 == 0 else 0
         self.dp_pool = torch.empty(max(ndp, 1) * te, dtype=torch.float64, device=dev)
         self.sp_pool = torch.empty(max(nsp, 1) * te, dtype=torch.float32, device=dev)
         self.scratch = torch.empty(max(nsc, 1) * te, dtype=torch.float32, device=dev)
         self.split = (torch.empty(nsl * te, dtype=torch.float32, device=dev) if nsl else None)
         self.dpanel = None
         if multi:
-            self.dpanel = torch.empty(lib.mt_dpanel_tiles_ex(self.p, self.row_stride,
-                                                             self.col_stride) * te,
-                                      dtype=torch.float64, device=dev)
+            self.dpanel = torch.empty(ndpn * te, dtype=torch.float64, device=dev)
         self.status = torch.empty(4, dtype=torch.int64, device=dev)
         self.desc = _lib.MtTiles(self.n, self.nb, self.p, t, mode, self.dp_pool.data_ptr(),
                                  self.sp_pool.data_ptr(), self.scratch.data_ptr(),
@@ -195,7 +197,7 @@ class TileMatrix:
                                  self.split.data_ptr() if self.split is not None else 0,
                                  self.col_stride, self.col_offset,
                                  self.dpanel.data_ptr() if self.dpanel is not None else 0,
-                                 self.row_stride, self.row_offset)
+                                 self.row_stride, self.row_offset, self.panel_slots)
         self.reset_status()
         self.tiles = _TileView(self)
 

@@ -328,3 +328,38 @@ def test_cluster_potrf_not_positive_definite_index(gpu):
             assert exc.value.index == 600
         finally:
             lib.mt_set_option(14, old)
+
+
+@pytest.mark.parametrize("n,nb,pol", [(8192, 512, "mp:3"), (5000, 256, "mp:1"), (4096, 256, "dp"),
+                                      (3000, 256, "dst:2")])
+def test_lookahead_two_bitwise(gpu, n, nb, pol):
+    """Lookahead depth 2 (panels k+1 and k+2 formed on the panel stream while
+    the bulk update applies step k; three ring slots) only moves work between
+    streams: factor, logdet and quad are bitwise equal to lookahead 0 and 1."""
+    import paper_2003_05324_b200 as mt
+    locs = mt.generate_locations(n, seed=43)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.random.default_rng(44).standard_normal(n)))
+    mode, _, t = pol.partition(":")
+    policy = (mt.PrecisionPolicy.dp() if mode == "dp" else
+              getattr(mt.PrecisionPolicy, mode)(diag_thick=int(t)))
+    th = mt.MaternParams(1.0, 0.1, 0.5)
+    asm = mt.TileAssembler(ds, nb)
+    outs, facs = [], []
+    for la in (0, 1, 2):
+        try:
+            outs.append(mt.Evaluator(asm, policy, lookahead=la)(th))
+        except mt.FactorizationError as exc:
+            outs.append(("npd", exc.index))
+        m = mt.TileMatrix(n, nb, policy, panel_slots=3 if la == 2 else 2)
+        asm.generate_into(m, th)
+        try:
+            facs.append(mt.cholesky(m, lookahead=la).tiles)
+        except mt.FactorizationError as exc:
+            facs.append(exc.index)
+    assert outs[0] == outs[1] == outs[2], outs
+    if isinstance(facs[0], int):
+        assert facs[0] == facs[1] == facs[2]
+        return
+    for key in facs[0]:
+        a, b, c = facs[0][key], facs[1][key], facs[2][key]
+        assert np.array_equal(a.dp, b.dp) and np.array_equal(a.dp, c.dp), key
