@@ -44,12 +44,21 @@ using namespace mt_pair;
 constexpr int BM = 128;   // accumulator rows per CTA (pair M = 256)
 constexpr int BN = 256;   // pair N (one MMA)
 constexpr int BNH = 128;  // rows of B each CTA stages
-constexpr int BK = 16;
+#ifndef MT_TCF_BK
+#define MT_TCF_BK 16
+#endif
+// K columns per operand slab: 16 (64-byte rows, SWIZZLE_64B) or 32 (128-byte
+// rows, SWIZZLE_128B: half the TMA row requests per byte, two slabs per stage
+// budget)
+constexpr int BK = MT_TCF_BK;
+static_assert(BK == 16 || BK == 32, "slab width");
+constexpr CUtensorMapSwizzle kSwz = BK == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
 #ifndef MT_TCF_KC
 #define MT_TCF_KC 2
 #endif
 constexpr int KC = MT_TCF_KC;  // K slabs per TMEM chunk
-static_assert(16 % KC == 0, "KC must divide the 16-slab item granularity");
+static_assert((256 / MT_TCF_BK) % KC == 0, "KC must divide the item's slab granularity");
+// (KC * BK = 32: the accumulator restarts every 32 K-columns at either slab width)
 #ifndef MT_TCF_STAGES
 #define MT_TCF_STAGES 4
 #endif
@@ -76,6 +85,13 @@ static_assert(SMEM_BYTES <= 232448, "shared memory");
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)(256 >> 4) << 24);
 
+// K-major UMMA smem descriptor of a swizzled operand slab: 8-row groups of
+// BK*4 bytes (SBO), layout SWIZZLE_64B (4) or SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t opdesc(const void* p) {
+  const uint64_t a = (smem_u32(p) >> 4) & 0x3FFF;
+  return a | ((uint64_t)((8 * BK * 4) >> 4) << 32) | (1ull << 46) |
+         ((uint64_t)(BK == 16 ? 4 : 2) << 61);
+}
 __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -340,9 +356,9 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const int off = kk * 32;
-              umma(dcol, sw64_desc(alo + off), sw64_desc(bhi + off), (c_first && kk == 0) ? 0u : 1u);
-              umma(dcol, sw64_desc(ahi + off), sw64_desc(blo + off), 1u);
-              umma(dcol, sw64_desc(ahi + off), sw64_desc(bhi + off), 1u);
+              umma(dcol, opdesc(alo + off), opdesc(bhi + off), (c_first && kk == 0) ? 0u : 1u);
+              umma(dcol, opdesc(ahi + off), opdesc(blo + off), 1u);
+              umma(dcol, opdesc(ahi + off), opdesc(bhi + off), 1u);
             }
             // stage s is free in every CTA that received part of it: both pairs
             // when B was multicast (each CTA's empty[s] then counts 2 commits)
@@ -589,9 +605,8 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   const int CL = (mt_opt_tcf_cluster4() && g.nb % (4 * BM) == 0) ? 4 : 2;
   CUtensorMap ma, mb, mc, ms;
   const int64_t split_rows = g.split_rows();
-  int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
-  if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, CL == 4 ? BNH / 2 : BNH,
-                            CU_TENSOR_MAP_SWIZZLE_64B);
+  int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, kSwz);
+  if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, CL == 4 ? BNH / 2 : BNH, kSwz);
   const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;
   if (!rc) rc = make_map_2d(&mc, g.sp ? (const void*)g.sp : (const void*)g.split, c_rows, g.nb, 4, 32,
                             32, CU_TENSOR_MAP_SWIZZLE_128B);
