@@ -353,13 +353,13 @@ def test_lookahead_two_bitwise(gpu, n, nb, pol):
         m = mt.TileMatrix(n, nb, policy, panel_slots=3 if la == 2 else 2)
         asm.generate_into(m, th)
         try:
-            facs.append(mt.cholesky(m, lookahead=la).tiles)
+            facs.append(mt.cholesky(m, lookahead=la))  # the factor keeps its matrix alive
         except mt.FactorizationError as exc:
             facs.append(exc.index)
     assert outs[0] == outs[1] == outs[2], outs
     if isinstance(facs[0], int):
         assert facs[0] == facs[1] == facs[2]
         return
-    for key in facs[0]:
-        a, b, c = facs[0][key], facs[1][key], facs[2][key]
+    for key in facs[0].tiles:
+        a, b, c = facs[0].tiles[key], facs[1].tiles[key], facs[2].tiles[key]
         assert np.array_equal(a.dp, b.dp) and np.array_equal(a.dp, c.dp), key
