@@ -12,7 +12,7 @@
 // FP32 FFMA / OpenBLAS sgemm (round-to-nearest) does not have
 // (tools/emulate_tf32x3.py, tools/emulate_flush.py).  The bias of a chunk
 // grows with its length, so each accumulation restarts from zero every KC
-// slabs (KC = 2: 4 MMA k-steps, K = 32) and the epilogue adds the chunk into
+// K=32 columns (KC slabs; 4 MMA k-steps) and the epilogue adds the chunk into
 // its registers with ordinary round-to-nearest FADDs; C_new = RN(C - sum).
 // CPU emulation of exactly this arithmetic puts kriging within 1.3x of the
 // reference's sgemm deviation from DP (RZ unflushed: 12.6x).
@@ -45,22 +45,23 @@ constexpr int BM = 128;   // accumulator rows per CTA (pair M = 256)
 constexpr int BN = 256;   // pair N (one MMA)
 constexpr int BNH = 128;  // rows of B each CTA stages
 #ifndef MT_TCF_BK
-#define MT_TCF_BK 16
+#define MT_TCF_BK 32
 #endif
-// K columns per operand slab: 16 (64-byte rows, SWIZZLE_64B) or 32 (128-byte
-// rows, SWIZZLE_128B: half the TMA row requests per byte, two slabs per stage
-// budget)
+// K columns per operand slab: 32 (128-byte rows, SWIZZLE_128B, 2 stages of
+// 64 KB; default) or 16 (64-byte rows, SWIZZLE_64B, 4 stages of 32 KB).  The
+// wider slab halves the TMA row requests per byte: 2.6% faster Cholesky at
+// N=262144, bitwise-identical results (profiles/ab_tcf_bk32_r02.txt)
 constexpr int BK = MT_TCF_BK;
 static_assert(BK == 16 || BK == 32, "slab width");
 constexpr CUtensorMapSwizzle kSwz = BK == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
 #ifndef MT_TCF_KC
-#define MT_TCF_KC 2
+#define MT_TCF_KC (32 / MT_TCF_BK)
 #endif
 constexpr int KC = MT_TCF_KC;  // K slabs per TMEM chunk
 static_assert((256 / MT_TCF_BK) % KC == 0, "KC must divide the item's slab granularity");
 // (KC * BK = 32: the accumulator restarts every 32 K-columns at either slab width)
 #ifndef MT_TCF_STAGES
-#define MT_TCF_STAGES 4
+#define MT_TCF_STAGES (MT_TCF_BK == 32 ? 2 : 4)
 #endif
 constexpr int STAGES = MT_TCF_STAGES;
 constexpr int A_BYTES = BM * BK * 4;                  // 8 KB
