@@ -11,8 +11,8 @@
 // biased roundings at the magnitude of the running sum -- a systematic error
 // FP32 FFMA / OpenBLAS sgemm (round-to-nearest) does not have
 // (tools/emulate_tf32x3.py, tools/emulate_flush.py).  The bias of a chunk
-// grows with its length, so each accumulation restarts from zero every KC
-// K=32 columns (KC slabs; 4 MMA k-steps) and the epilogue adds the chunk into
+// grows with its length, so each accumulation restarts from zero every 32
+// K-columns (KC slabs; 4 MMA k-steps) and the epilogue adds the chunk into
 // its registers with ordinary round-to-nearest FADDs; C_new = RN(C - sum).
 // CPU emulation of exactly this arithmetic puts kriging within 1.3x of the
 // reference's sgemm deviation from DP (RZ unflushed: 12.6x).
