@@ -8,8 +8,9 @@ log-likelihood evaluation at N = 262,144 locations, tile 512, MP band t = 8,
 Matern (1, 0.1, 0.5) on a Morton-sorted synthetic field -- covariance
 generation -> band-precision tile Cholesky -> logdet -> quadratic form, all on
 the device.  MP at this size needs 142 GB, so it fits one B200; with N > 1 the
-same evaluation is split over the ranks (tile-column-cyclic layout, NCCL panel
-broadcasts; strong scaling).  Prints ONE JSON line (rank 0).
+same evaluation is split over the ranks (2D block-cyclic P x Q tiles, NCCL
+row/column panel broadcasts; strong scaling).  `--gpus N` outside torchrun
+spawns the N ranks itself.  Prints ONE JSON line (rank 0).
 
   value      whole-job loglik evaluations/s, inputs resident in HBM, device time
              (CUDA events on the launching stream, max over ranks).
@@ -18,13 +19,16 @@ broadcasts; strong scaling).  Prints ONE JSON line (rank 0).
              (`loglik_distributed` for N > 1) from pinned host buffers: H2D of
              locations + z and D2H of the result inside the timed region.
   roofline   dominant kernel (the tcgen05 3xTF32 bulk update): algorithmic
-             flops per launch / average launch duration from CUDA events
-             recorded around every launch inside the timed region; plus the
-             flop-weighted FP64/FP32 roofline of the whole factorization.
+             flops per launch / the launches' device-side span inside the
+             timed region (frac raw; the per-SM-share figure beside it); plus
+             the flop-weighted FP64/FP32 roofline of the whole factorization
+             (P64 = FP64 DMMA probe of this run, sustained).
   mp_vs_dp   the build's own full-DP path timed the same way (at N = 262144
              when it fits the ranks' memory, else at configs[1] N = 65536).
   cpu_baseline  the reference algorithm (oracle port: same LAPACK/BLAS calls as
-             the reference) on the host cores, bounded sample, extrapolated.
+             the reference) on the host cores, bounded sample at N = 16384,
+             extrapolated by component (assembly/solve N^2, FP64/FP32 kernels
+             by planned flops at their measured rates, task loop p^3).
 
 --impl reference times only the CPU reference arm (rank 0).
 """
@@ -479,11 +483,10 @@ def run_ours(args, rank, world, local_rank):
                      "update on the same stream, so stream events cannot bracket it); "
                      "algorithmic flops = reference flop model (factor.py:83-95) per launch"),
         "share_of_step": d["ms"] / (t_dev / args.steps * 1e3),
-        "traffic_source": ("profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk-update "
-                           "launch (tc2w_update_kernel, one evaluation at the bench config); above "
-                           "the algorithmic C read+write "
-                           "because the A-panel rows are re-fetched per output column (the panel, "
-                           "2 MB/tile, exceeds L2); the kernel is tensor-bound at ~54% of HBM "
+        "traffic_source": (f"profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk-update "
+                           f"launch ({dom_kernel}, one evaluation at the bench config); above "
+                           "the algorithmic C read+write because the A-panel rows are re-fetched "
+                           "per output column (the panel, 2 MB/tile, exceeds L2); ~45% of HBM "
                            "bandwidth (DESIGN.md section 4)"),
         "cholesky_flop_weighted": {
             "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
