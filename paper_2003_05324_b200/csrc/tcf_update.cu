@@ -73,8 +73,16 @@ constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 #ifndef MT_TCF_CSLOTS
 #define MT_TCF_CSLOTS 3
 #endif
-// C-chunk slots per epilogue warp (2 or 3; 2 leaves room for a 5th operand stage)
-constexpr int CSLOTS = MT_TCF_CSLOTS, CSLOT_BYTES = 32 * 32 * 4;
+#ifndef MT_TCF_CW
+#define MT_TCF_CW 32
+#endif
+// C chunks: 32 rows x CW columns (CW = 32: 128-byte rows, SWIZZLE_128B; 16:
+// 64-byte rows, SWIZZLE_64B); CSLOTS per epilogue warp (2 or 3)
+constexpr int CW = MT_TCF_CW, NE = CW / 4;  // NE: 16-byte groups per chunk row
+static_assert(CW == 32 || CW == 16, "C chunk width");
+constexpr int NCW = COLS_W / CW;  // C chunks per warp and item
+constexpr CUtensorMapSwizzle kSwzC = CW == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+constexpr int CSLOTS = MT_TCF_CSLOTS, CSLOT_BYTES = 32 * CW * 4;
 static_assert(CSLOTS == 2 || CSLOTS == 3, "C-chunk slots");
 constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 96 KB at 3 slots
 constexpr int TMEM_COLS = 512;                               // 2 chunk buffers x 256 columns
@@ -110,6 +118,11 @@ __device__ __forceinline__ void ld32(uint32_t (&v)[32], uint32_t taddr) {
         "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// physical 16-byte group of group e in row `row` of a swizzled C chunk
+// (16-byte-group index XOR address bits 7..9 for 128 B rows, 7..8 for 64 B rows)
+__device__ __forceinline__ int swz(int e, int row) {
+  return CW == 32 ? (e ^ (row & 7)) : (e ^ ((row >> 1) & 3));
 }
 __device__ __forceinline__ void ld16(uint32_t (&v)[16], uint32_t taddr) {
   asm volatile(
@@ -433,20 +446,20 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           // C of this item: slots free once the previous item's stores were read
           bulk_wait_read<0>();
           if (out == OUT_UPDATE) {
-            for (int m = 0; m < CSLOTS; ++m) load_c(m, n0 + m * 32, crow);
-            for (int m = CSLOTS; m < 4; ++m) prefetch_l2_2d(&map_c, n0 + m * 32, crow);
+            for (int m = 0; m < CSLOTS; ++m) load_c(m, n0 + m * CW, crow);
+            for (int m = CSLOTS; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
           } else {
             load_c(0, n0, crow);
-            for (int m = 1; m < 4; ++m) prefetch_l2_2d(&map_c, n0 + m * 32, crow);
+            for (int m = 1; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
           }
         }
       }
-      // ---- output: lane = row, 32 columns per chunk m, SWIZZLE_128B slots
-      // x[0..31] -> slot s row `lane`: the values (part 0), or their TF32 hi (1) / lo (2)
+      // ---- output: lane = row, CW columns per chunk m, swizzled slots
+      // x[0..CW-1] -> slot s row `lane`: the values (part 0), or their TF32 hi (1) / lo (2)
       auto put = [&](int s, const float* x, int part) {
-        const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * 128;
+        const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * (CW * 4);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < NE; ++e) {
           float y[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -454,56 +467,56 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
             mt_tf32_split(x[4 * e + u], h, l);
             y[u] = part == 0 ? x[4 * e + u] : (part == 1 ? h : l);
           }
-          sts128(rowa + ((e ^ (lane & 7)) << 4), make_float4(y[0], y[1], y[2], y[3]));
+          sts128(rowa + (swz(e, lane) << 4), make_float4(y[0], y[1], y[2], y[3]));
         }
       };
       if (out == OUT_UPDATE) {
 #pragma unroll
-        for (int m = 0; m < COLS_W / 32; ++m) {
+        for (int m = 0; m < NCW; ++m) {
           const int s = m % CSLOTS;
           wait_c(s);
-          const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * 128;
+          const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * (CW * 4);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t a = rowa + ((e ^ (lane & 7)) << 4);
+          for (int e = 0; e < NE; ++e) {
+            const uint32_t a = rowa + (swz(e, lane) << 4);
             float4 cc = lds128(a);
-            cc.x -= sum[32 * m + 4 * e];
-            cc.y -= sum[32 * m + 4 * e + 1];
-            cc.z -= sum[32 * m + 4 * e + 2];
-            cc.w -= sum[32 * m + 4 * e + 3];
+            cc.x -= sum[CW * m + 4 * e];
+            cc.y -= sum[CW * m + 4 * e + 1];
+            cc.z -= sum[CW * m + 4 * e + 2];
+            cc.w -= sum[CW * m + 4 * e + 3];
             sts128(a, cc);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * 32, crow);
+            tma_store_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * CW, crow);
             bulk_commit();
-            if (m + CSLOTS < 4) {  // chunk m + CSLOTS reuses this slot (L2-prefetched)
+            if (m + CSLOTS < NCW) {  // chunk m + CSLOTS reuses this slot (L2-prefetched)
               bulk_wait_read<0>();
-              load_c(s, n0 + (m + CSLOTS) * 32, crow);
+              load_c(s, n0 + (m + CSLOTS) * CW, crow);
             }
           }
         }
       } else {
 #pragma unroll
-        for (int m = 0; m < COLS_W / 32; ++m) {
-          float x[32];
+        for (int m = 0; m < NCW; ++m) {
+          float x[CW];
           if (out == OUT_PRESPLIT) {
             wait_c(0);
-            const uint32_t rowa = smem_u32(slots) + lane * 128;
+            const uint32_t rowa = smem_u32(slots) + lane * (CW * 4);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float4 cc = lds128(rowa + ((e ^ (lane & 7)) << 4));
-              x[4 * e] = cc.x - sum[32 * m + 4 * e];
-              x[4 * e + 1] = cc.y - sum[32 * m + 4 * e + 1];
-              x[4 * e + 2] = cc.z - sum[32 * m + 4 * e + 2];
-              x[4 * e + 3] = cc.w - sum[32 * m + 4 * e + 3];
+            for (int e = 0; e < NE; ++e) {
+              const float4 cc = lds128(rowa + (swz(e, lane) << 4));
+              x[4 * e] = cc.x - sum[CW * m + 4 * e];
+              x[4 * e + 1] = cc.y - sum[CW * m + 4 * e + 1];
+              x[4 * e + 2] = cc.z - sum[CW * m + 4 * e + 2];
+              x[4 * e + 3] = cc.w - sum[CW * m + 4 * e + 3];
             }
           } else {
             if (lane == 0) bulk_wait_read<0>();  // slots free (previous chunk's stores read)
             __syncwarp();
 #pragma unroll
-            for (int u = 0; u < 32; ++u) x[u] = sum[32 * m + u];
+            for (int u = 0; u < CW; ++u) x[u] = sum[CW * m + u];
           }
           put(0, x, 0);
           put(1, x, 1);
@@ -511,9 +524,9 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&map_c, slots, n0 + m * 32, crow);
-            tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * 32, srow);
-            if (CSLOTS > 2) tma_store_2d(&map_s, slots + 2 * CSLOT_BYTES, n0 + m * 32, srow + nb);
+            tma_store_2d(&map_c, slots, n0 + m * CW, crow);
+            tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * CW, srow);
+            if (CSLOTS > 2) tma_store_2d(&map_s, slots + 2 * CSLOT_BYTES, n0 + m * CW, srow + nb);
             bulk_commit();
           }
           if (CSLOTS == 2) {  // the TF32 lo part goes through slot 1 once hi was read
@@ -523,14 +536,14 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * 32, srow + nb);
+              tma_store_2d(&map_s, slots + CSLOT_BYTES, n0 + m * CW, srow + nb);
               bulk_commit();
             }
           }
           if (lane == 0) {
-            if (out == OUT_PRESPLIT && m < 3) {
+            if (out == OUT_PRESPLIT && m < NCW - 1) {
               bulk_wait_read<0>();
-              load_c(0, n0 + (m + 1) * 32, crow);
+              load_c(0, n0 + (m + 1) * CW, crow);
             }
           }
           __syncwarp();
@@ -609,9 +622,9 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   int rc = make_map_2d(&ma, g.split, split_rows, g.nb, 4, BK, BM, kSwz);
   if (!rc) rc = make_map_2d(&mb, g.split, split_rows, g.nb, 4, BK, CL == 4 ? BNH / 2 : BNH, kSwz);
   const int64_t c_rows = g.noff() > 0 ? g.noff() * g.nb : 32;
-  if (!rc) rc = make_map_2d(&mc, g.sp ? (const void*)g.sp : (const void*)g.split, c_rows, g.nb, 4, 32,
-                            32, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = make_map_2d(&ms, g.split, split_rows, g.nb, 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_map_2d(&mc, g.sp ? (const void*)g.sp : (const void*)g.split, c_rows, g.nb, 4, CW,
+                            32, kSwzC);
+  if (!rc) rc = make_map_2d(&ms, g.split, split_rows, g.nb, 4, CW, 32, kSwzC);
   if (rc) return rc;
   WorkF w;
   w.slot0 = s0;
