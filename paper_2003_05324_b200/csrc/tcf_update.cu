@@ -47,10 +47,12 @@ constexpr int BNH = 128;  // rows of B each CTA stages
 #ifndef MT_TCF_BK
 #define MT_TCF_BK 32
 #endif
-// K columns per operand slab: 32 (128-byte rows, SWIZZLE_128B, 2 stages of
-// 64 KB; default) or 16 (64-byte rows, SWIZZLE_64B, 4 stages of 32 KB).  The
-// wider slab halves the TMA row requests per byte: 2.6% faster Cholesky at
-// N=262144, bitwise-identical results (profiles/ab_tcf_bk32_r02.txt)
+// K columns per operand slab: 32 (128-byte rows, SWIZZLE_128B; default) or
+// 16 (64-byte rows, SWIZZLE_64B).  The wider slab halves the TMA row requests
+// per byte.  Same-box A/B at N=262144 (bitwise-identical results,
+// profiles/ab_tcf_stages_r02.txt): 16-column slabs x 4 stages + 3 C slots of
+// 32 columns 40.10 s; 32 x 2 + 3 x 32 38.99 s; 32 x 3 + 2 C slots of 16
+// columns 37.81 s (default)
 constexpr int BK = MT_TCF_BK;
 static_assert(BK == 16 || BK == 32, "slab width");
 constexpr CUtensorMapSwizzle kSwz = BK == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
@@ -61,7 +63,7 @@ constexpr int KC = MT_TCF_KC;  // K slabs per TMEM chunk
 static_assert((256 / MT_TCF_BK) % KC == 0, "KC must divide the item's slab granularity");
 // (KC * BK = 32: the accumulator restarts every 32 K-columns at either slab width)
 #ifndef MT_TCF_STAGES
-#define MT_TCF_STAGES (MT_TCF_BK == 32 ? 2 : 4)
+#define MT_TCF_STAGES (MT_TCF_BK == 32 ? 3 : 4)
 #endif
 constexpr int STAGES = MT_TCF_STAGES;
 constexpr int A_BYTES = BM * BK * 4;                  // 8 KB
@@ -71,10 +73,10 @@ constexpr int EPI_WARPS = 8;
 constexpr int COLS_W = BN / 2;  // columns per epilogue warp
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 #ifndef MT_TCF_CSLOTS
-#define MT_TCF_CSLOTS 3
+#define MT_TCF_CSLOTS (MT_TCF_BK == 32 ? 2 : 3)
 #endif
 #ifndef MT_TCF_CW
-#define MT_TCF_CW 32
+#define MT_TCF_CW (MT_TCF_BK == 32 ? 16 : 32)
 #endif
 // C chunks: 32 rows x CW columns (CW = 32: 128-byte rows, SWIZZLE_128B; 16:
 // 64-byte rows, SWIZZLE_64B); CSLOTS per epilogue warp (2 or 3)
