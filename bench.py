@@ -608,7 +608,9 @@ def run_ours(args, rank, world, local_rank):
             "library_options": opts or "defaults", "fp32_engine": engine,
             "nccl": ({"version": ".".join(map(str, torch.cuda.nccl.version())),
                       "world_size": world, "backend": dist.get_backend(),
-                      "init_lines": nccl_summary()} if dist_on else None),
+                      "grid": list(grid),
+                      "debug": (f"NCCL_DEBUG={os.environ.get('NCCL_DEBUG')} "
+                                f"(INIT lines on stderr)")} if dist_on else None),
             "loglik_sample": results[-1],
         }
         print(json.dumps(line), flush=True)
@@ -634,31 +636,12 @@ def spawn_ranks(args):
 
 
 def nccl_debug_env():
-    """NCCL's communicator-init lines (rank count, transports, NVLS) go to a
-    per-process file, not to stdout (which carries the JSON line)."""
+    """NCCL's communicator-init lines (rank count, transports, NVLS) go to
+    stderr, where the driver can count the ranks; stdout carries only the
+    JSON line."""
     os.environ.setdefault("NCCL_DEBUG", "INFO")
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-    os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(
-        os.environ.get("MT_NCCL_LOG_DIR", "/tmp"), "mt_bench_nccl.%h.%p.log"))
-
-
-def nccl_summary():
-    """Init lines of this run's NCCL logs (rank 0 reports them)."""
-    import glob
-    pat = os.environ.get("NCCL_DEBUG_FILE", "").replace("%h", "*").replace("%p", "*")
-    lines = []
-    for f in sorted(glob.glob(pat)) if pat else []:
-        try:
-            if os.path.getmtime(f) < _T_START:
-                continue
-            with open(f) as fh:
-                lines += [ln.strip() for ln in fh if "Init COMPLETE" in ln or "nranks" in ln]
-        except OSError:
-            pass
-    return lines[:16]
-
-
-_T_START = time.time()
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 
 def run_dry(args, rank, world):
