@@ -27,6 +27,13 @@ def _data(n):
     return g["locs"][:n], g["z"][:n]
 
 
+def _policy(mt, tag):
+    if tag == "dp":
+        return mt.PrecisionPolicy.dp()
+    mode, t = tag.split(":")
+    return getattr(mt.PrecisionPolicy, mode)(diag_thick=int(t))
+
+
 def _worker(rank, world, port, n, nb, tag, queue, grid=None):
     import torch
     import torch.distributed as dist
@@ -37,9 +44,14 @@ def _worker(rank, world, port, n, nb, tag, queue, grid=None):
     from paper_2003_05324_b200.distributed import DistributedEvaluator
     locs, z = _data(n)
     ds = mt.GeoDataset(locs, z)
-    pol = mt.PrecisionPolicy.dp() if tag == "dp" else mt.PrecisionPolicy.mp(diag_thick=int(tag[3:]))
+    pol = _policy(mt, tag)
     ev = DistributedEvaluator(mt.TileAssembler(ds, nb), pol, grid=grid)
-    ld, quad = ev(mt.MaternParams(1.0, 0.1, 0.5))
+    try:
+        ld, quad = ev(mt.MaternParams(1.0, 0.1, 0.5))
+    except mt.FactorizationError as exc:  # (DST may be indefinite: same pivot everywhere)
+        queue.put((rank, "npd", exc.index, None))
+        dist.destroy_process_group()
+        return
     tiles = {key: (t.dp, t.sp) for key, t in ev.matrix.tiles.items()}
     queue.put((rank, ld, quad, tiles))
     dist.destroy_process_group()
@@ -47,7 +59,7 @@ def _worker(rank, world, port, n, nb, tag, queue, grid=None):
 
 @pytest.mark.parametrize("tag,grid", [("mp:2", (1, 2)), ("dp", (1, 2)), ("mp:1", (1, 2)),
                                       ("mp:2", (2, 2)), ("dp", (2, 2)), ("mp:3", (2, 1)),
-                                      ("mp:2", (2, 1))])
+                                      ("mp:2", (2, 1)), ("dst:2", (2, 2))])
 def test_ranks_bitwise_equal_single_gpu(gpu, tag, grid):
     """1 x 2, 2 x 1 and 2 x 2 process grids (2D block-cyclic tiles, row and
     column sub-communicators): factor, logdet and quad bitwise equal to one GPU."""
@@ -71,9 +83,13 @@ def test_ranks_bitwise_equal_single_gpu(gpu, tag, grid):
         pr.join(timeout=120)
         assert pr.exitcode == 0
     locs, z = _data(n)
-    pol = mt.PrecisionPolicy.dp() if tag == "dp" else mt.PrecisionPolicy.mp(diag_thick=int(tag[3:]))
+    pol = _policy(mt, tag)
     ev = mt.Evaluator(mt.TileAssembler(mt.GeoDataset(locs, z), nb), pol, lookahead=1)
-    ld1, q1 = ev(mt.MaternParams(1.0, 0.1, 0.5))
+    try:
+        ld1, q1 = ev(mt.MaternParams(1.0, 0.1, 0.5))
+    except mt.FactorizationError as exc:
+        assert all(r[1] == "npd" and r[2] == exc.index for r in res), (exc.index, res)
+        return
     ref = ev.matrix.tiles
     seen = set()
     for rank, ld, quad, tiles in res:
