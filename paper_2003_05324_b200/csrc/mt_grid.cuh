@@ -214,38 +214,43 @@ struct Grid {
 // before row x number P(x) = G(x, ma) - G(x, mb) with
 // G(x, a) = sum_{i<x} max(0, floor((i - d_a) / cs)), d_a = t + c0 + (a - 1) cs,
 // = T(x - d_a) - T(-d_a),  T(Y) = sum_{y<Y} floor(y / cs)  (0 for Y <= 0).
-__device__ __forceinline__ int64_t stair_T(int64_t y, int cs) {
+// 32-bit arithmetic: the work-queue owner maps one item per call, and 64-bit
+// divisions in a loop over super-columns made that mapping (~10 us per item at
+// p = 512) slower than an item's MMA time -- the super-column order then lost
+// to slot order (round-2 A/B).  Super-column starts are scol() differences
+// (O(1)); one binary search picks the super-column, one the row.
+__device__ __forceinline__ int stair_T(int y, int cs) {
   if (y <= 0) return 0;
-  const int64_t q = y / cs, r = y % cs;
-  return (int64_t)cs * q * (q - 1) / 2 + r * q;
+  const int q = y / cs, r = y - q * cs;
+  return cs * (q * (q - 1) / 2) + r * q;
 }
-__device__ __forceinline__ int64_t stair_G(const Grid& g, int64_t x, int a) {
-  const int64_t d = (int64_t)g.t + g.c0 + (int64_t)(a - 1) * g.cs;
+__device__ __forceinline__ int stair_G(const Grid& g, int x, int a) {
+  const int d = g.t + g.c0 + (a - 1) * g.cs;
   return stair_T(x - d, g.cs) - stair_T(-d, g.cs);
 }
-__device__ __forceinline__ int64_t super_prefix(const Grid& g, int64_t x, int ma, int mb) {
+__device__ __forceinline__ int super_prefix(const Grid& g, int x, int ma, int mb) {
   return stair_G(g, x, ma) - stair_G(g, x, mb);
 }
 // tile index -> (i, j) in super-column order over owned columns [mlo, mhi)
-__device__ __forceinline__ void super_tile_ij(const Grid& g, int64_t idx, int mlo, int mhi, int sw, int& i,
-                              int& j) {
-  int ma = mlo;
-  for (;;) {
-    const int mb = min(mhi, ma + sw);
-    const int64_t cnt = super_prefix(g, g.p, ma, mb);
-    if (idx < cnt || mb >= mhi) {
-      int lo = 0, hi = g.p;  // largest row x with P(x) <= idx
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (super_prefix(g, mid, ma, mb) <= idx) lo = mid; else hi = mid;
-      }
-      i = lo;
-      j = g.owned_col(ma + (int)(idx - super_prefix(g, lo, ma, mb)));
-      return;
-    }
-    idx -= cnt;
-    ma = mb;
+// (single process row: rs == 1)
+__device__ __forceinline__ void super_tile_ij(const Grid& g, int64_t idx64, int mlo, int mhi, int sw,
+                                              int& i, int& j) {
+  const int idx = (int)idx64;
+  const int base = (int)g.scol(g.owned_col(mlo));
+  int lo = 0, hi = (mhi - mlo + sw - 1) / sw;  // largest super-column s starting at <= idx
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if ((int)g.scol(g.owned_col(mlo + mid * sw)) - base <= idx) lo = mid; else hi = mid;
   }
+  const int ma = mlo + lo * sw, mb = min(mhi, ma + sw);
+  const int local = idx - ((int)g.scol(g.owned_col(ma)) - base);
+  int rlo = 0, rhi = g.p;  // largest row x with P(x) <= local
+  while (rhi - rlo > 1) {
+    const int mid = (rlo + rhi) >> 1;
+    if (super_prefix(g, mid, ma, mb) <= local) rlo = mid; else rhi = mid;
+  }
+  i = rlo;
+  j = g.owned_col(ma + (local - super_prefix(g, rlo, ma, mb)));
 }
 
 
