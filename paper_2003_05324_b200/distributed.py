@@ -40,6 +40,7 @@ from .factor import FactorizationError
 from .tilestore import PrecisionOverflowError, TileMatrix
 
 LOG_2PI = math.log(2.0 * math.pi)
+_GROUPS = {}  # (member ranks, P, Q) -> (row groups, column groups)
 
 
 # --------------------------------------------------------------- grid plan
@@ -136,13 +137,19 @@ class DistributedEvaluator:
         members = (dist.get_process_group_ranks(group) if group is not None
                    else list(range(self.world)))
         self.members = members
-        # sub-communicators: every rank creates every group, in the same order
+        # sub-communicators: every rank creates every group, in the same order;
+        # cached per (members, grid) so repeated evaluators (loglik_distributed,
+        # fit loops) do not re-create NCCL communicators
         self.row_groups, self.col_groups = [], []
         if self.P > 1 and self.Q > 1:
-            self.row_groups = [dist.new_group([members[r * self.Q + c] for c in range(self.Q)])
-                               for r in range(self.P)]
-            self.col_groups = [dist.new_group([members[r * self.Q + c] for r in range(self.P)])
-                               for c in range(self.Q)]
+            key = (tuple(members), self.P, self.Q)
+            if key not in _GROUPS:
+                _GROUPS[key] = (
+                    [dist.new_group([members[r * self.Q + c] for c in range(self.Q)])
+                     for r in range(self.P)],
+                    [dist.new_group([members[r * self.Q + c] for r in range(self.P)])
+                     for c in range(self.Q)])
+            self.row_groups, self.col_groups = _GROUPS[key]
         elif self.Q > 1:
             self.row_groups = [group]
         elif self.P > 1:
