@@ -301,7 +301,8 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   4: CTAs of the lookahead panel-column FP32 update (0 = all SMs)
  *   5: SMs the bulk FP32 update yields to the panel kernels on request (0 = off)
  *   6: super-column width (owned tile columns) of the bulk FP32 update's output
- *      order, for L2 reuse of the panel operands (0 = column-by-column slot order)
+ *      order, for L2 reuse of the panel operands (default 8; 0 = column-by-column
+ *      slot order; single process row only)
  *   7: 1 = the FP32 update prefetches each work item's C block into L2 when the
  *      item is dequeued (cp.async.bulk.prefetch.L2), 0 = off
  *   8: diagnostics of the FP32 update epilogue (timing only, WRONG results):

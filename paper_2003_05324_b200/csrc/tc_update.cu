@@ -441,7 +441,7 @@ int launch_tc32(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool t
                          span, jlo, jhi);
   // full-width (256 x 512) CTA-pair items for the bulk update (tc2w_update.cu)
   if (!trsm && mt_opt_wide_items() && mt_opt_cta_pairs() && mt_tc2w_supported(g) && jlo > k + 1 &&
-      !mt_opt_tc_diag() && !mt_opt_c_prefetch() && mt_opt_super_cols() == 0)
+      !mt_opt_tc_diag() && !mt_opt_c_prefetch())
     return mt_tc2w_launch(g, k, s0, scnt, ctas, st, span);
   if (mt_opt_cta_pairs() && !mt_opt_tc_diag() && !mt_opt_c_prefetch())  // CTA-pair kernel
     return mt_tc2_launch(g, k, s0, scnt, ctas, trsm,
