@@ -303,12 +303,7 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   6: super-column width (owned tile columns) of the bulk FP32 update's output
  *      order, for L2 reuse of the panel operands (default 8; 0 = column-by-column
  *      slot order; single process row only)
- *   7: 1 = the FP32 update prefetches each work item's C block into L2 when the
- *      item is dequeued (cp.async.bulk.prefetch.L2), 0 = off
- *   8: diagnostics of the FP32 update epilogue (timing only, WRONG results):
- *      bit 0 skip C loads, bit 1 skip C stores, bit 2 skip the epilogue
- *   9: 1 = FP32 update and off-band TRSM on CTA pairs (tcgen05.mma.cta_group::2,
- *      M = 256, each CTA stages half of B; default), 0 = single-CTA kernel
+ *   7, 8, 9: retired (round-1 single-CTA tcgen05 kernel A/B switches; -1)
  *  10: 1 = co-schedule the FP64 band update (programmatic dependent launch) on the
  *      SMs a capped bulk FP32 update leaves free (default), 0 = one after the other
  *  11: band update's SM share under option 10, in % of its work share (default 90)

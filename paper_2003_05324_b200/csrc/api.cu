@@ -297,9 +297,6 @@ static int g_coschedule = 1;   // 1 = band DMMA update co-scheduled beside the c
 static int g_cosched_pct = 90; // band update's SM share, % of its work share (option 11)
 static int g_wide_items = 1;   // 1 = bulk FP32 update on 256 x 512 pair items (nb % 512 == 0)
 static int g_wide_l2pf = 0;    // 1 = the 256 x 512 update stages each warp's C rows in L2
-static int g_cta_pairs = 1;    // 1 = FP32 update/TRSM on CTA pairs (tcgen05 cta_group::2)
-static int g_tc_diag = 0;      // diagnostics (wrong results): 1 no C loads, 2 no C stores, 4 no epilogue
-static int g_c_prefetch = 0;   // 1 = FP32 update stages each item's C block in L2 (cp.async.bulk.prefetch)
 static int g_tcf_stats = 0;     // 1 = tcf kernels accumulate MMA-issuer wait cycles (diagnostics)
 static int g_tcf_cluster4 = 0;  // 1 = RN tcgen05 update on 4-CTA clusters (B multicast across two pairs)
 static int g_potrf_cluster = 0;  // 1 = POTRF on a cluster of nb/32 CTAs (tile in distributed smem; opt-in)
@@ -310,9 +307,6 @@ int mt_opt_tc_trsm() { return g_tc_trsm; }
 int mt_opt_pcol_ctas() { return g_pcol_ctas; }
 int mt_opt_yield_sms() { return g_yield_sms; }
 int mt_opt_super_cols() { return g_super_cols; }
-int mt_opt_c_prefetch() { return g_c_prefetch; }
-int mt_opt_tc_diag() { return g_tc_diag; }
-int mt_opt_cta_pairs() { return g_cta_pairs; }
 int mt_opt_wide_items() { return g_wide_items; }
 int mt_opt_wide_l2pf() { return g_wide_l2pf; }
 int mt_opt_coschedule() { return g_coschedule; }
@@ -334,11 +328,7 @@ int32_t mt_version(void) { return 11; }
  * option 4: CTAs of the lookahead panel-column FP32 update (0 = all SMs);
  * option 5: SMs the bulk FP32 update yields to the panel TRSM (0 = off);
  * option 6: super-column width of the FP32 update's output order (default 8, 0 = slot order);
- * option 7: 1 = the FP32 update prefetches each work item's C block into L2;
- * option 8: diagnostics of the FP32 update epilogue (WRONG RESULTS, timing only):
- *           bit 0 skip C loads, bit 1 skip C stores, bit 2 skip the epilogue;
- * option 9: 1 = FP32 update / off-band TRSM on CTA pairs (tcgen05.mma.cta_group::2,
- *           default), 0 = single-CTA kernel.
+ * options 7-9: retired (round-1 single-CTA kernel A/B switches);
  * Returns the old value. */
 int32_t mt_set_option(int32_t option, int32_t value) {
   int old = -1;
@@ -349,9 +339,6 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 4) { old = g_pcol_ctas; g_pcol_ctas = value; }
   else if (option == 5) { old = g_yield_sms; g_yield_sms = value; }
   else if (option == 6) { old = g_super_cols; g_super_cols = value; }
-  else if (option == 7) { old = g_c_prefetch; g_c_prefetch = value; }
-  else if (option == 8) { old = g_tc_diag; g_tc_diag = value; }
-  else if (option == 9) { old = g_cta_pairs; g_cta_pairs = value; }
   else if (option == 10) { old = g_coschedule; g_coschedule = value; }
   else if (option == 11) { old = g_cosched_pct; g_cosched_pct = value; }
   else if (option == 12) { old = g_wide_items; g_wide_items = value; }

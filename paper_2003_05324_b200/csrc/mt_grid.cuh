@@ -358,9 +358,6 @@ int mt_opt_tc_trsm();
 int mt_tc_update_impl(const Grid& g, int k, int jlo, int jhi, int ctas, cudaStream_t st,
                       unsigned long long* span = nullptr);
 int mt_opt_super_cols();
-int mt_opt_c_prefetch();
-int mt_opt_tc_diag();
-int mt_opt_cta_pairs();
 int mt_opt_wide_items();
 int mt_opt_wide_l2pf();
 bool mt_tc2w_supported(const Grid& g);

@@ -416,7 +416,7 @@ int mt_update_impl(const Grid& g, int k, int jlo, int jhi, cudaStream_t st) {
   const int64_t co_b0 = g.bcol(jlo), co_bcnt = g.bcol(jhi) - co_b0;
   if (mt_opt_coschedule() && !pcol && g.mode == MT_MODE_MP && co_scnt > 0 && co_bcnt > 0 &&
       (mt_engine_tc(mt_opt_engine()) || g.multi()) && mt_tc_supported(g) &&
-      mt_opt_cta_pairs() && mt_opt_legacy_dmma() != 1 && mt_dmma_tma_supported(g)) {
+      mt_opt_legacy_dmma() != 1 && mt_dmma_tma_supported(g)) {
     static int sms = 0;
     if (!sms) {
       int dev = 0;

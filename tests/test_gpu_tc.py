@@ -211,35 +211,6 @@ def test_sm_yield_keeps_results_bitwise(gpu, ysms):
         assert np.array_equal(a.dp, b.dp), key
 
 
-@pytest.mark.parametrize("n,nb,t,ysms", [(4096, 256, 2, 0), (6144, 512, 3, 32), (3000, 256, 1, 200)])
-def test_cta_pair_kernel_bitwise_equals_single_cta(rz_engine, n, nb, t, ysms):
-    """The CTA-pair (tcgen05.mma.cta_group::2, M=256) FP32 update and off-band
-    TRSM apply the same MMA sequence to every output element as the
-    single-CTA kernel: factors are bit-identical (option 9), with and without
-    the SM-yield protocol, including a ragged last tile."""
-    mt = _mt()
-    from paper_2003_05324_b200 import _lib
-    lib = _lib.load()
-    locs = mt.generate_locations(n, seed=17)
-    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
-    pol = mt.PrecisionPolicy.mp(diag_thick=t)
-    facs = []
-    oy = lib.mt_set_option(5, ysms)
-    try:
-        for pairs in (0, 1):
-            old = lib.mt_set_option(9, pairs)
-            try:
-                facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5),
-                                                               nb, pol), lookahead=1))
-            finally:
-                lib.mt_set_option(9, old)
-    finally:
-        lib.mt_set_option(5, oy)
-    for key in facs[0].tiles:
-        a, b = facs[0].tiles[key], facs[1].tiles[key]
-        assert np.array_equal(a.dp, b.dp), key
-
-
 @pytest.mark.parametrize("n,nb,t", [(8192, 512, 3), (6144, 256, 2)])
 def test_coscheduled_band_update_bitwise(gpu, n, nb, t):
     """Option 10 (FP64 band update launched as a programmatic dependent beside a
