@@ -81,11 +81,12 @@ constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 // C chunks: 32 rows x CW columns (CW = 32: 128-byte rows, SWIZZLE_128B; 16:
 // 64-byte rows, SWIZZLE_64B); CSLOTS per epilogue warp (2 or 3)
 constexpr int CW = MT_TCF_CW, NE = CW / 4;  // NE: 16-byte groups per chunk row
-static_assert(CW == 32 || CW == 16, "C chunk width");
+static_assert(CW == 32 || CW == 16 || CW == 8, "C chunk width");
 constexpr int NCW = COLS_W / CW;  // C chunks per warp and item
-constexpr CUtensorMapSwizzle kSwzC = CW == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+constexpr CUtensorMapSwizzle kSwzC = CW == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                    : (CW == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 constexpr int CSLOTS = MT_TCF_CSLOTS, CSLOT_BYTES = 32 * CW * 4;
-static_assert(CSLOTS == 2 || CSLOTS == 3, "C-chunk slots");
+static_assert(CSLOTS >= 2 && CSLOTS <= 4, "C-chunk slots");
 constexpr int EPI_BYTES = EPI_WARPS * CSLOTS * CSLOT_BYTES;  // 96 KB at 3 slots
 constexpr int TMEM_COLS = 512;                               // 2 chunk buffers x 256 columns
 constexpr int SCHED = 4;
@@ -122,9 +123,10 @@ __device__ __forceinline__ void ld32(uint32_t (&v)[32], uint32_t taddr) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 // physical 16-byte group of group e in row `row` of a swizzled C chunk
-// (16-byte-group index XOR address bits 7..9 for 128 B rows, 7..8 for 64 B rows)
+// (16-byte-group index XOR address bits 7..9 for 128 B rows, 7..8 for 64 B
+// rows, 7 for 32 B rows)
 __device__ __forceinline__ int swz(int e, int row) {
-  return CW == 32 ? (e ^ (row & 7)) : (e ^ ((row >> 1) & 3));
+  return CW == 32 ? (e ^ (row & 7)) : (CW == 16 ? (e ^ ((row >> 1) & 3)) : (e ^ ((row >> 2) & 1)));
 }
 __device__ __forceinline__ void ld16(uint32_t (&v)[16], uint32_t taddr) {
   asm volatile(
