@@ -307,10 +307,11 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *  10: 1 = co-schedule the FP64 band update (programmatic dependent launch) on the
  *      SMs a capped bulk FP32 update leaves free (default), 0 = one after the other
  *  11: band update's SM share under option 10, in % of its work share (default 90)
- *  14: 1 = POTRF on a cluster of nb/32 CTAs with the tile in distributed shared
- *      memory (bitwise equal to the single-CTA kernel; 0.75 vs 1.37 ms per
- *      512-tile alone, but a 16-CTA cluster waits for a free GPC beside the
- *      co-scheduled bulk update: opt-in, default 0)
+ *  14: POTRF variant, all bitwise equal: 0 = one CTA (default); 1 = a cluster of
+ *      nb/32 CTAs with the tile in distributed shared memory (0.75 vs 1.37 ms
+ *      per 512-tile alone, but a 16-CTA cluster waits for a free GPC beside
+ *      the co-scheduled bulk update); 2 = three small launches per 32-column
+ *      block (no co-residency requirement)
  *  12: 1 = bulk FP32 update on full-width 256 x 512 CTA-pair items (two N=256 MMAs
  *      per product, single-buffered TMEM; needs nb % 512 == 0; default), 0 = 256 x 256 items
  *  13: 1 = the 256 x 512 update prefetches each epilogue warp's C rows into L2 */

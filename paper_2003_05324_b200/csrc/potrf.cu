@@ -394,6 +394,157 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Multi-kernel POTRF (option 14 = 2): per 32-column block cb three small
+// launches -- the diagonal block (1 CTA: warp-shuffle pivots + CTA inverse),
+// the panel blocks (one CTA per row block below), the trailing lower blocks
+// (one CTA per (c, q) block pair) -- with the single-CTA kernel's operation
+// order per element (bitwise equal).  No cluster and no co-residency: every
+// launch takes whatever SMs are free beside the bulk update, so the serial
+// chain is the diagonal-block work plus launch latency.
+__global__ void __launch_bounds__(kThreads) potrf_mk_diag(Grid g, int k, int cb, int narrow) {
+  if (g.failed()) return;
+  double* __restrict__ A = g.dtile(k, k);
+  const int nb = g.nb, c0 = cb * 32;
+  __shared__ double Ld[32][33];
+  __shared__ double Li[32][33];
+  __shared__ double part[8][33];
+  __shared__ int bad;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) bad = -1;
+  __syncthreads();
+  if (warp == 0) {
+    const int r = lane;
+    double a[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = c <= r ? A[(int64_t)(c0 + r) * nb + c0 + c] : 0.0;
+    int fail = -1;
+#pragma unroll 1
+    for (int j = 0; j < 32; ++j) {
+      double piv = __shfl_sync(0xffffffffu, a[0], j);
+      if (fail < 0 && !(piv > 0.0)) fail = j;
+      if (fail >= 0) piv = 1.0;
+      const double d = sqrt(piv);
+      double lrj = a[0];
+      if (r == j) lrj = d;
+      else if (r > j) lrj = lrj / d;
+      Ld[r][j] = r >= j ? lrj : 0.0;
+#pragma unroll
+      for (int cc = 1; cc < 32; ++cc) {
+        const double lcj = __shfl_sync(0xffffffffu, lrj, (j + cc) & 31);
+        if (j + cc < 32 && r >= j + cc) a[cc] -= lrj * lcj;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 31; ++cc) a[cc] = a[cc + 1];
+      a[31] = 0.0;
+    }
+    if (fail >= 0 && lane == 0) bad = c0 + fail;
+  }
+  __syncthreads();
+  if (bad >= 0) {
+    if (threadIdx.x == 0)
+      atomicCAS((unsigned long long*)&g.status[MT_ST_PIVOT], (unsigned long long)-1LL,
+                (unsigned long long)((int64_t)k * nb + bad));
+    return;
+  }
+  const int ci = threadIdx.x & 31, pt = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int r = 0; r < 32; ++r) {
+    double sacc = 0.0;
+    for (int q = ci + pt; q < r; q += 8) sacc += Ld[r][q] * Li[q][ci];
+    part[pt][ci] = sacc;
+    __syncthreads();
+    if (pt == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += part[u][ci];
+      Li[r][ci] = r < ci ? 0.0 : (r == ci ? 1.0 / Ld[r][r] : -t / Ld[r][r]);
+    }
+    __syncthreads();
+  }
+  float* S = narrow ? g.sdiag(k) : nullptr;
+  double* inv64 = g.sinv64(k);
+  float* inv32 = g.sinv32(k);
+  for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
+    const int r = e >> 5, c = e & 31;
+    if (c <= r) {
+      const int64_t o = (int64_t)(c0 + r) * nb + c0 + c;
+      A[o] = Ld[r][c];
+      if (S) S[o] = __double2float_rn(Ld[r][c]);
+    }
+    inv64[cb * 1024 + e] = Li[r][c];
+    inv32[cb * 1024 + e] = __double2float_rn(Li[r][c]);
+  }
+}
+
+// panel block (c, cb), c = cb + 1 + blockIdx.x: X = A[c, cb] Li^T
+__global__ void __launch_bounds__(kThreads) potrf_mk_panel(Grid g, int k, int cb, int narrow) {
+  if (g.failed()) return;
+  double* __restrict__ A = g.dtile(k, k);
+  const int nb = g.nb, c0 = cb * 32, r0 = (cb + 1 + blockIdx.x) * 32;
+  __shared__ double Li[32][33];
+  __shared__ double X[32][33];
+  const double* inv64 = g.sinv64(k) + cb * 1024;
+  for (int e = threadIdx.x; e < 1024; e += kThreads) {
+    Li[e >> 5][e & 31] = inv64[e];
+    X[e >> 5][e & 31] = A[(int64_t)(r0 + (e >> 5)) * nb + c0 + (e & 31)];
+  }
+  __syncthreads();
+  const int rr = threadIdx.x >> 3, cg = (threadIdx.x & 7) * 4;
+  double o[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int q = 0; q < 32; ++q) {
+    const double av = X[rr][q];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) o[u] += av * Li[cg + u][q];
+  }
+  float* S = narrow ? g.sdiag(k) : nullptr;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t off = (int64_t)(r0 + rr) * nb + c0 + cg + u;
+    A[off] = o[u];
+    if (S) S[off] = __double2float_rn(o[u]);
+  }
+}
+
+// trailing block (c, q), cb < q <= c: A[c, q] -= X_c X_q^T on DMMA
+__global__ void __launch_bounds__(kThreads) potrf_mk_trail(Grid g, int k, int cb) {
+  if (g.failed()) return;
+  double* __restrict__ A = g.dtile(k, k);
+  const int nb = g.nb, c0 = cb * 32;
+  // blockIdx.x -> (tr, tc), tc <= tr, over the m = nblk - cb - 1 trailing row blocks
+  const int tIdx = blockIdx.x;
+  int tr = (int)((sqrtf(8.0f * (float)tIdx + 1.0f) - 1.0f) * 0.5f);
+  while (tr * (tr + 1) / 2 > tIdx) --tr;
+  while ((tr + 1) * (tr + 2) / 2 <= tIdx) ++tr;
+  const int tc = tIdx - tr * (tr + 1) / 2;
+  const int rc = (cb + 1 + tr) * 32, rq = (cb + 1 + tc) * 32;
+  __shared__ double Xc[32][PLD];
+  __shared__ double Xq[32][PLD];
+  for (int e = threadIdx.x; e < 1024; e += kThreads) {
+    Xc[e >> 5][e & 31] = A[(int64_t)(rc + (e >> 5)) * nb + c0 + (e & 31)];
+    Xq[e >> 5][e & 31] = A[(int64_t)(rq + (e >> 5)) * nb + c0 + (e & 31)];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fm = warp >> 1, fn0 = (warp & 1) * 2;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int k4 = 0; k4 < 32; k4 += 4) {
+    const double af = Xc[fm * 8 + (lane >> 2)][k4 + (lane & 3)];
+#pragma unroll
+    for (int f = 0; f < 2; ++f) dmma884(acc[f], af, Xq[(fn0 + f) * 8 + (lane >> 2)][k4 + (lane & 3)]);
+  }
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int r = fm * 8 + (lane >> 2), c = (fn0 + f) * 8 + 2 * (lane & 3);
+    double* cp = A + (int64_t)(rc + r) * nb + rq + c;
+    if (tr != tc || c <= r) cp[0] -= acc[f][0];
+    if (tr != tc || c + 1 <= r) cp[1] -= acc[f][1];
+  }
+}
+
 }  // namespace
 
 static size_t potrf_cluster_smem(int nb) {
@@ -406,10 +557,23 @@ static int g_potrf_cluster = -1;  // -1 unknown, 0 unavailable, 1 usable
 
 int mt_potrf_impl(const Grid& g, int k, int narrow, cudaStream_t st) {
   const double r = g.rows(k);
-  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0,
-               (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)));
   const int nblk = g.nb / 32;
-  if (mt_opt_potrf_cluster() && g.nb % 32 == 0 && nblk >= 2 && nblk <= 16 &&
+  const bool multi_kernel = mt_opt_potrf_cluster() == 2 && g.nb % 32 == 0 && nblk >= 2;
+  ProfScope ps(MT_K_POTRF, st, r * r * r / 3.0,
+               (double)g.nb * g.nb * (16.0 + (narrow ? 4.0 : 0.0)), multi_kernel ? 3 * nblk - 2 : 1);
+  if (multi_kernel) {
+    for (int cb = 0; cb < nblk; ++cb) {
+      potrf_mk_diag<<<1, kThreads, 0, st>>>(g, k, cb, narrow);
+      const int m = nblk - cb - 1;
+      if (m > 0) {
+        potrf_mk_panel<<<m, kThreads, 0, st>>>(g, k, cb, narrow);
+        potrf_mk_trail<<<m * (m + 1) / 2, kThreads, 0, st>>>(g, k, cb);
+      }
+    }
+    MT_LAUNCH_CHECK("potrf_mk");
+    return MT_OK;
+  }
+  if (mt_opt_potrf_cluster() == 1 && g.nb % 32 == 0 && nblk >= 2 && nblk <= 16 &&
       potrf_cluster_smem(g.nb) <= 220 * 1024 && g_potrf_cluster != 0) {
     const size_t smem = potrf_cluster_smem(g.nb);
     cudaFuncSetAttribute(potrf_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -280,9 +280,10 @@ def test_fused_forward_sweep_bitwise(gpu, n, nb, t, la):
                                       (1920, 128, "dst:2")])
 def test_cluster_potrf_bitwise_equals_single_cta(gpu, n, nb, pol):
     """Option 14: POTRF on a cluster of nb/32 CTAs (tile in distributed shared
-    memory) applies the single-CTA kernel's operations in the same order: the
-    factor (including the FP32 narrowing and the 32x32 inverses feeding the
-    TRSM) is bitwise identical; ragged last tile included."""
+    memory) or as three small launches per 32-column block applies the
+    single-CTA kernel's operations in the same order: the factor (including
+    the FP32 narrowing and the 32x32 inverses feeding the TRSM) is bitwise
+    identical; ragged last tile included."""
     import paper_2003_05324_b200 as mt
     from paper_2003_05324_b200 import _lib
     lib = _lib.load()
@@ -292,7 +293,7 @@ def test_cluster_potrf_bitwise_equals_single_cta(gpu, n, nb, pol):
     policy = (mt.PrecisionPolicy.dp() if mode == "dp" else
               getattr(mt.PrecisionPolicy, mode)(diag_thick=int(t)))
     facs = []
-    for flag in (0, 1):
+    for flag in (0, 1, 2):
         old = lib.mt_set_option(14, flag)
         try:
             facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5), nb,
@@ -302,12 +303,13 @@ def test_cluster_potrf_bitwise_equals_single_cta(gpu, n, nb, pol):
         finally:
             lib.mt_set_option(14, old)
     if not hasattr(facs[0], "tiles"):
-        assert facs[0] == facs[1]
+        assert facs[0] == facs[1] == facs[2]
         return
-    for key in facs[0].tiles:
-        a, b = facs[0].tiles[key], facs[1].tiles[key]
-        assert np.array_equal(a.dp, b.dp), key
-        assert (a.sp is None) == (b.sp is None) and (a.sp is None or np.array_equal(a.sp, b.sp))
+    for other in facs[1:]:
+        for key in facs[0].tiles:
+            a, b = facs[0].tiles[key], other.tiles[key]
+            assert np.array_equal(a.dp, b.dp), key
+            assert (a.sp is None) == (b.sp is None) and (a.sp is None or np.array_equal(a.sp, b.sp))
 
 
 def test_cluster_potrf_not_positive_definite_index(gpu):
@@ -320,7 +322,7 @@ def test_cluster_potrf_not_positive_definite_index(gpu):
     x = rng.standard_normal((n, n))
     a = x @ x.T / n + np.eye(n)
     a[600, 600] = -5.0
-    for flag in (0, 1):
+    for flag in (0, 1, 2):
         old = lib.mt_set_option(14, flag)
         try:
             with pytest.raises(mt.FactorizationError) as exc:
