@@ -4,7 +4,7 @@
 // One CTA (8 warps) walks the tile in 32-wide column blocks, right-looking:
 //   1. warp 0 factors the 32x32 diagonal block with the rows held in
 //      registers (lane r owns row r, pivots broadcast by shuffles, no CTA
-//      barrier per pivot), then the CTA forms its triangular inverse;
+//      barrier per pivot) and forms its triangular inverse column-wise;
 //   2. the sub-diagonal panel is solved as a parallel GEMM against that
 //      inverse (X = A L_dd^{-T}), staged in shared memory;
 //   3. the trailing lower triangle takes the rank-32 SYRK update on the FP64
@@ -30,6 +30,65 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// 32x32 diagonal block: factor and triangular inverse, by ONE warp, no CTA
+// barrier.  Lane r loads row r (rows/columns >= w are the identity) and the
+// fully unrolled right-looking pivot loop keeps every index static: pivot j
+// is broadcast by a shuffle, d = sqrt(pivot), the column is scaled by the
+// reciprocal 1/d (dpotf2: DSCAL by ONE/AJJ) and the trailing entries of the
+// row take a[c] -= L[r][j] L[c][j], j ascending.  The inverse is then formed
+// column-wise, lane c holding column c of L^{-1}: x_r = b_r / L[r][r] (as the
+// product with the pivot's reciprocal, already in every lane) and
+// b_q -= L[q][r] x_r for q > r, the L column read by broadcast from Ld.
+// Writes Ld (lower, zero above; column 32 = the pivot reciprocals) and Li
+// (lower, zero above) in shared memory (row stride 33); returns the local
+// index of the first non-positive / NaN pivot, -1 when the block is positive
+// definite (warp-uniform).  Every POTRF variant calls this, so their results
+// stay bitwise equal.  ncu at N=65536: potrf_kernel 1.37 -> 1.00 ms per tile,
+// the cluster kernel 0.75 -> 0.35 ms, against the former shuffle pivots + a
+// CTA-wide row-by-row inverse (64 barriers); a rolled pivot loop (window
+// shifted through the registers) measured 1.12 / 0.44 ms.
+__device__ __noinline__ int diag_block_factor_inverse(const double* src, int64_t ld, int w,
+                                                        double* Ld, double* Li) {
+  const int r = threadIdx.x & 31;
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    a[c] = (r < w && c < w) ? (c <= r ? src[r * ld + c] : 0.0) : (r == c ? 1.0 : 0.0);
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double piv = __shfl_sync(0xffffffffu, a[j], j);
+    if (fail < 0 && !(piv > 0.0)) fail = j;  // warp-uniform; later steps are discarded
+    if (fail >= 0) piv = 1.0;
+    const double d = sqrt(piv);
+    const double rd = 1.0 / d;
+    if (r == 0) Ld[j * 33 + 32] = rd;  // the pad column keeps 1 / L[j][j]
+    const double lrj = r == j ? d : (r > j ? a[j] * rd : 0.0);
+    a[j] = lrj;
+#pragma unroll
+    for (int c = j + 1; c < 32; ++c) {
+      const double lcj = __shfl_sync(0xffffffffu, lrj, c);  // L[c][j]
+      if (r >= c) a[c] -= lrj * lcj;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) Ld[r * 33 + c] = c <= r ? a[c] : 0.0;
+  __syncwarp();
+  // inverse: lane c solves L x = e_c (reuses a[] as b / x)
+#pragma unroll
+  for (int q = 0; q < 32; ++q) a[q] = q == r ? 1.0 : 0.0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    a[q] = q < r ? 0.0 : a[q] * Ld[q * 33 + 32];
+#pragma unroll
+    for (int u = q + 1; u < 32; ++u) a[u] -= Ld[u * 33 + q] * a[q];
+  }
+#pragma unroll
+  for (int q = 0; q < 32; ++q) Li[q * 33 + r] = a[q];
+  __syncwarp();
+  return fail;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int narrow) {
   if (g.failed()) return;
   double* __restrict__ A = g.dtile(k, k);
@@ -45,60 +104,13 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int n
 
   for (int c0 = 0, blk = 0; c0 < nb; c0 += 32, ++blk) {
     const int w = min(32, nb - c0);
-    // ---------------- 1. diagonal block: factor (warp 0) + inverse (CTA) --
-    // Warp 0 factors the block with lane r holding row r in registers: the 32
-    // dependent pivot steps use shuffles and __syncwarp-free register updates
-    // instead of three CTA barriers each.  a[cc] is column j + cc of the row
-    // (the window shifts left after every pivot, so indices stay static).
+    // ---------------- 1. diagonal block: factor + inverse (warp 0) ---------
     if (warp == 0) {
-      const int r = lane;
-      double a[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        a[c] = (r < w && c < w) ? (c <= r ? A[(int64_t)(c0 + r) * nb + c0 + c] : 0.0)
-                                : (r == c ? 1.0 : 0.0);
-      int fail = -1;
-#pragma unroll 1
-      for (int j = 0; j < 32; ++j) {
-        double piv = __shfl_sync(0xffffffffu, a[0], j);
-        if (fail < 0 && !(piv > 0.0)) fail = j;  // warp-uniform; later steps are discarded
-        if (fail >= 0) piv = 1.0;
-        const double d = sqrt(piv);
-        double lrj = a[0];
-        if (r == j) lrj = d;
-        else if (r > j) lrj = lrj / d;
-        Ld[r][j] = r >= j ? lrj : 0.0;
-#pragma unroll
-        for (int cc = 1; cc < 32; ++cc) {
-          const double lcj = __shfl_sync(0xffffffffu, lrj, (j + cc) & 31);  // L[j+cc][j]
-          if (j + cc < 32 && r >= j + cc) a[cc] -= lrj * lcj;
-        }
-#pragma unroll
-        for (int cc = 0; cc < 31; ++cc) a[cc] = a[cc + 1];
-        a[31] = 0.0;
-      }
+      const int fail = diag_block_factor_inverse(A + (int64_t)c0 * nb + c0, nb, w, &Ld[0][0], &Li[0][0]);
       if (fail >= 0 && lane == 0) bad = c0 + fail;
     }
     __syncthreads();
     if (bad < 0) {
-      // inverse of the 32x32 factor, row by row: thread (c, part) of 32 x 8
-      // forms a partial dot, parts are reduced in fixed order
-      __shared__ double part[8][33];
-      const int ci = threadIdx.x & 31, pt = threadIdx.x >> 5;
-#pragma unroll 1
-      for (int r = 0; r < 32; ++r) {
-        double s = 0.0;
-        for (int q = ci + pt; q < r; q += 8) s += Ld[r][q] * Li[q][ci];
-        part[pt][ci] = s;
-        __syncthreads();
-        if (pt == 0) {
-          double t = 0.0;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) t += part[u][ci];
-          Li[r][ci] = r < ci ? 0.0 : (r == ci ? 1.0 / Ld[r][r] : -t / Ld[r][r]);
-        }
-        __syncthreads();
-      }
       // write the factored block (lower), its FP32 narrowing, and the inverse
       float* S = narrow ? g.sdiag(k) : nullptr;
       for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
@@ -225,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_kernel(Grid g, int k, int n
 // of nb/32 CTAs (one SM each), the tile resident in distributed shared memory.
 // CTA c holds row block c (its 32 x 32(c+1) lower part).  For each column
 // block cb: CTA cb factors its diagonal block and forms the inverse (the same
-// warp-shuffle pivots and CTA inverse as potrf_kernel); after a cluster
+// diagonal-block factor and inverse as potrf_kernel); after a cluster
 // barrier every CTA c > cb solves its panel block X_c = A[c,cb] Li^T; after a
 // second barrier it applies A[c,q] -= X_c X_q^T for cb < q <= c on DMMA,
 // reading X_q from CTA q's shared memory.  Every element sees the same
@@ -251,7 +263,6 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int 
   double* Lp = Li + 32 * 33;                     // [32][33] peer's inverse (copy)
   double* Xq = Lp + 32 * 33;                     // [32][36] peer's panel block (copy)
   __shared__ int bad;
-  __shared__ double part[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* A = g.dtile(k, k);
   double* inv64 = g.sinv64(k);
@@ -273,49 +284,11 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int 
     if (c == cb) {
       // -------- diagonal block: warp 0 factors it in registers (potrf_kernel step 1)
       if (warp == 0) {
-        const int r = lane;
-        double a[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) a[q] = q <= r ? Dcb[r * ld + q] : 0.0;
-        int fail = -1;
-#pragma unroll 1
-        for (int j = 0; j < 32; ++j) {
-          double piv = __shfl_sync(0xffffffffu, a[0], j);
-          if (fail < 0 && !(piv > 0.0)) fail = j;
-          if (fail >= 0) piv = 1.0;
-          const double d = sqrt(piv);
-          double lrj = a[0];
-          if (r == j) lrj = d;
-          else if (r > j) lrj = lrj / d;
-          Ld[r * 33 + j] = r >= j ? lrj : 0.0;
-#pragma unroll
-          for (int cc = 1; cc < 32; ++cc) {
-            const double lcj = __shfl_sync(0xffffffffu, lrj, (j + cc) & 31);
-            if (j + cc < 32 && r >= j + cc) a[cc] -= lrj * lcj;
-          }
-#pragma unroll
-          for (int cc = 0; cc < 31; ++cc) a[cc] = a[cc + 1];
-          a[31] = 0.0;
-        }
+        const int fail = diag_block_factor_inverse(Dcb, ld, 32, Ld, Li);
         if (fail >= 0 && lane == 0) bad = cb * 32 + fail;
       }
       __syncthreads();
       if (bad < 0) {
-        const int ci = threadIdx.x & 31, pt = threadIdx.x >> 5;
-#pragma unroll 1
-        for (int r = 0; r < 32; ++r) {
-          double sacc = 0.0;
-          for (int q = ci + pt; q < r; q += 8) sacc += Ld[r * 33 + q] * Li[q * 33 + ci];
-          part[pt][ci] = sacc;
-          __syncthreads();
-          if (pt == 0) {
-            double t = 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) t += part[u][ci];
-            Li[r * 33 + ci] = r < ci ? 0.0 : (r == ci ? 1.0 / Ld[r * 33 + r] : -t / Ld[r * 33 + r]);
-          }
-          __syncthreads();
-        }
         for (int e = threadIdx.x; e < 32 * 32; e += kThreads) {
           const int r = e >> 5, q = e & 31;
           if (q <= r) Dcb[r * ld + q] = Ld[r * 33 + q];
@@ -397,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) potrf_cluster_kernel(Grid g, int 
 
 // ---------------------------------------------------------------------------
 // Multi-kernel POTRF (option 14 = 2): per 32-column block cb three small
-// launches -- the diagonal block (1 CTA: warp-shuffle pivots + CTA inverse),
+// launches -- the diagonal block (1 CTA: one warp factors and inverts it),
 // the panel blocks (one CTA per row block below), the trailing lower blocks
 // (one CTA per (c, q) block pair) -- with the single-CTA kernel's operation
 // order per element (bitwise equal).  No cluster and no co-residency: every
@@ -409,36 +382,12 @@ __global__ void __launch_bounds__(kThreads) potrf_mk_diag(Grid g, int k, int cb,
   const int nb = g.nb, c0 = cb * 32;
   __shared__ double Ld[32][33];
   __shared__ double Li[32][33];
-  __shared__ double part[8][33];
   __shared__ int bad;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) bad = -1;
   __syncthreads();
   if (warp == 0) {
-    const int r = lane;
-    double a[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) a[c] = c <= r ? A[(int64_t)(c0 + r) * nb + c0 + c] : 0.0;
-    int fail = -1;
-#pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-      double piv = __shfl_sync(0xffffffffu, a[0], j);
-      if (fail < 0 && !(piv > 0.0)) fail = j;
-      if (fail >= 0) piv = 1.0;
-      const double d = sqrt(piv);
-      double lrj = a[0];
-      if (r == j) lrj = d;
-      else if (r > j) lrj = lrj / d;
-      Ld[r][j] = r >= j ? lrj : 0.0;
-#pragma unroll
-      for (int cc = 1; cc < 32; ++cc) {
-        const double lcj = __shfl_sync(0xffffffffu, lrj, (j + cc) & 31);
-        if (j + cc < 32 && r >= j + cc) a[cc] -= lrj * lcj;
-      }
-#pragma unroll
-      for (int cc = 0; cc < 31; ++cc) a[cc] = a[cc + 1];
-      a[31] = 0.0;
-    }
+    const int fail = diag_block_factor_inverse(A + (int64_t)c0 * nb + c0, nb, 32, &Ld[0][0], &Li[0][0]);
     if (fail >= 0 && lane == 0) bad = c0 + fail;
   }
   __syncthreads();
@@ -447,21 +396,6 @@ __global__ void __launch_bounds__(kThreads) potrf_mk_diag(Grid g, int k, int cb,
       atomicCAS((unsigned long long*)&g.status[MT_ST_PIVOT], (unsigned long long)-1LL,
                 (unsigned long long)((int64_t)k * nb + bad));
     return;
-  }
-  const int ci = threadIdx.x & 31, pt = threadIdx.x >> 5;
-#pragma unroll 1
-  for (int r = 0; r < 32; ++r) {
-    double sacc = 0.0;
-    for (int q = ci + pt; q < r; q += 8) sacc += Ld[r][q] * Li[q][ci];
-    part[pt][ci] = sacc;
-    __syncthreads();
-    if (pt == 0) {
-      double t = 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) t += part[u][ci];
-      Li[r][ci] = r < ci ? 0.0 : (r == ci ? 1.0 / Ld[r][r] : -t / Ld[r][r]);
-    }
-    __syncthreads();
   }
   float* S = narrow ? g.sdiag(k) : nullptr;
   double* inv64 = g.sinv64(k);
