@@ -307,14 +307,19 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *  10: 1 = co-schedule the FP64 band update (programmatic dependent launch) on the
  *      SMs a capped bulk FP32 update leaves free (default), 0 = one after the other
  *  11: band update's SM share under option 10, in % of its work share (default 90)
+ *  12: (round-1 RZ engine) 1 = bulk FP32 update on full-width 256 x 512 CTA-pair
+ *      items (needs nb % 512 == 0; default), 0 = 256 x 256 items
+ *  13: (round-1 RZ engine) 1 = the 256 x 512 update prefetches C rows into L2
  *  14: POTRF variant, all bitwise equal: 0 = one CTA (default); 1 = a cluster of
- *      nb/32 CTAs with the tile in distributed shared memory (0.75 vs 1.37 ms
+ *      nb/32 CTAs with the tile in distributed shared memory (0.35 vs 1.00 ms
  *      per 512-tile alone, but a 16-CTA cluster waits for a free GPC beside
  *      the co-scheduled bulk update); 2 = three small launches per 32-column
  *      block (no co-residency requirement)
- *  12: 1 = bulk FP32 update on full-width 256 x 512 CTA-pair items (two N=256 MMAs
- *      per product, single-buffered TMEM; needs nb % 512 == 0; default), 0 = 256 x 256 items
- *  13: 1 = the 256 x 512 update prefetches each epilogue warp's C rows into L2 */
+ *  15: 1 = FP32 update on clusters of two CTA pairs sharing the B operand
+ *  16: 1 = FP32 update diagnostics (mt_tcf_stats)
+ *  17: 1 = the FP32 update applies C -= sum as a TMA reduce-add of -sum at L2
+ *      (no C load round trip at the end of each item; bitwise equal; default),
+ *      0 = C loaded into shared memory, C - sum stored */
 int32_t mt_set_option(int32_t option, int32_t value);
 
 /* Fill *theta from (variance, range, smoothness) on the host (covmath.py:72-95). */

@@ -297,6 +297,7 @@ static int g_coschedule = 1;   // 1 = band DMMA update co-scheduled beside the c
 static int g_cosched_pct = 90; // band update's SM share, % of its work share (option 11)
 static int g_wide_items = 1;   // 1 = bulk FP32 update on 256 x 512 pair items (nb % 512 == 0)
 static int g_wide_l2pf = 0;    // 1 = the 256 x 512 update stages each warp's C rows in L2
+static int g_tcf_reduce = 1;    // 1 = tcf update applies C -= sum as a TMA reduce-add (no C load; default)
 static int g_tcf_stats = 0;     // 1 = tcf kernels accumulate MMA-issuer wait cycles (diagnostics)
 static int g_tcf_cluster4 = 0;  // 1 = RN tcgen05 update on 4-CTA clusters (B multicast across two pairs)
 static int g_potrf_cluster = 0;  // 1 = POTRF on a cluster of nb/32 CTAs (tile in distributed smem; opt-in)
@@ -314,6 +315,7 @@ int mt_opt_coschedule_pct() { return g_cosched_pct; }
 int mt_opt_potrf_cluster() { return g_potrf_cluster; }
 int mt_opt_tcf_cluster4() { return g_tcf_cluster4; }
 int mt_opt_tcf_stats() { return g_tcf_stats; }
+int mt_opt_tcf_reduce() { return g_tcf_reduce; }
 
 extern "C" {
 
@@ -346,6 +348,7 @@ int32_t mt_set_option(int32_t option, int32_t value) {
   else if (option == 14) { old = g_potrf_cluster; g_potrf_cluster = value; }
   else if (option == 15) { old = g_tcf_cluster4; g_tcf_cluster4 = value; }
   else if (option == 16) { old = g_tcf_stats; g_tcf_stats = value; }
+  else if (option == 17) { old = g_tcf_reduce; g_tcf_reduce = value; }
   return old;
 }
 const char* mt_last_error(void) { return g_err; }

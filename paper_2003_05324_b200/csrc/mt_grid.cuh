@@ -351,6 +351,7 @@ int mt_opt_coschedule_pct();
 int mt_opt_potrf_cluster();
 int mt_opt_tcf_cluster4();
 int mt_opt_tcf_stats();
+int mt_opt_tcf_reduce();
 bool mt_tc_supported(const Grid& g);
 bool mt_tc_trsm_enabled(const Grid& g);  // off-band TRSM as a tcgen05 GEMM against L_kk^{-1}
 int mt_tc_trsm_impl(const Grid& g, int k, cudaStream_t st);

@@ -173,6 +173,7 @@ struct WorkF {
   unsigned long long* span;
   int mlo, mhi, sw;  // update: owned column range, super-column width (0 = slot order)
   int stats;         // option 16: accumulate MMA-issuer wait cycles
+  int red;           // option 17: C -= sum as a TMA reduce-add of -sum (no C load)
 };
 
 enum { OUT_UPDATE = 0, OUT_PRESPLIT = 1, OUT_TRSM = 2 };
@@ -448,11 +449,15 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
         ++ch;
         if (c == 0 && out != OUT_TRSM && lane == 0) {
           // C of this item: slots free once the previous item's stores were read
-          bulk_wait_read<0>();
-          if (out == OUT_UPDATE) {
+          if (out == OUT_UPDATE && w.red) {
+            // the reduce-adds at the end of the item find C in L2
+            for (int m = 0; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
+          } else if (out == OUT_UPDATE) {
+            bulk_wait_read<0>();
             for (int m = 0; m < CSLOTS; ++m) load_c(m, n0 + m * CW, crow);
             for (int m = CSLOTS; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
           } else {
+            bulk_wait_read<0>();
             load_c(0, n0, crow);
             for (int m = 1; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
           }
@@ -474,7 +479,33 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           sts128(rowa + (swz(e, lane) << 4), make_float4(y[0], y[1], y[2], y[3]));
         }
       };
-      if (out == OUT_UPDATE) {
+      if (out == OUT_UPDATE && w.red) {
+        // C - sum == C + (-sum) in IEEE arithmetic: the TMA unit adds -sum into
+        // C at L2, the warp only waits for a slot's previous reduce to have
+        // read its source (chunk 0: every earlier bulk op of this warp, which
+        // may have used the slots in another pattern)
+#pragma unroll
+        for (int m = 0; m < NCW; ++m) {
+          const int s = m % CSLOTS;
+          if (lane == 0) {
+            if (m == 0) bulk_wait_read<0>();
+            else bulk_wait_read<CSLOTS - 1>();
+          }
+          __syncwarp();
+          const uint32_t rowa = smem_u32(slots + s * CSLOT_BYTES) + lane * (CW * 4);
+#pragma unroll
+          for (int e = 0; e < NE; ++e)
+            sts128(rowa + (swz(e, lane) << 4),
+                   make_float4(-sum[CW * m + 4 * e], -sum[CW * m + 4 * e + 1],
+                               -sum[CW * m + 4 * e + 2], -sum[CW * m + 4 * e + 3]));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * CW, crow);
+            bulk_commit();
+          }
+        }
+      } else if (out == OUT_UPDATE) {
 #pragma unroll
         for (int m = 0; m < NCW; ++m) {
           const int s = m % CSLOTS;
@@ -641,6 +672,7 @@ int mt_tcf_launch(const Grid& g, int k, int64_t s0, int64_t scnt, int ctas, bool
   w.mhi = g.owned_before(jhi);
   w.sw = (!trsm && jhi > jlo + 1 && g.rs == 1) ? mt_opt_super_cols() : 0;
   w.stats = mt_opt_tcf_stats();
+  w.red = mt_opt_tcf_reduce();
   int dev = 0;
   cudaGetDevice(&dev);
   if (!g_smf) cudaDeviceGetAttribute(&g_smf, cudaDevAttrMultiProcessorCount, dev);

@@ -287,3 +287,32 @@ def test_tcf_four_cta_clusters_bitwise(gpu, n, t, co):
         lib.mt_set_option(10, oc)
     for key in facs[0].tiles:
         assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
+
+
+@pytest.mark.parametrize("n,t,co,c4", [(8192, 3, 1, 0), (7000, 2, 0, 0), (12288, 8, 1, 1)])
+def test_tcf_reduce_add_bitwise(gpu, n, t, co, c4):
+    """Option 17: the FP32 update writes -sum and lets the TMA unit add it into
+    C at L2 (C + (-sum) == C - sum in IEEE arithmetic) instead of loading C
+    into shared memory and storing C - sum: bitwise equal factors, panel-column
+    updates with the fused TF32 split and ragged last tiles included."""
+    mt = _mt()
+    from paper_2003_05324_b200 import _lib
+    lib = _lib.load()
+    locs = mt.generate_locations(n, seed=41)
+    ds, _ = mt.morton_sort(mt.GeoDataset(locs, np.zeros(n)))
+    pol = mt.PrecisionPolicy.mp(diag_thick=t)
+    facs = []
+    oc, o4 = lib.mt_set_option(10, co), lib.mt_set_option(15, c4)
+    try:
+        for red in (0, 1):
+            old = lib.mt_set_option(17, red)
+            try:
+                facs.append(mt.cholesky(mt.assemble_covariance(ds, mt.MaternParams(1.0, 0.1, 0.5),
+                                                               512, pol), lookahead=1))
+            finally:
+                lib.mt_set_option(17, old)
+    finally:
+        lib.mt_set_option(10, oc)
+        lib.mt_set_option(15, o4)
+    for key in facs[0].tiles:
+        assert np.array_equal(facs[0].tiles[key].dp, facs[1].tiles[key].dp), key
