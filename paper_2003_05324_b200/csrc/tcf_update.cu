@@ -69,8 +69,12 @@ constexpr int STAGES = MT_TCF_STAGES;
 constexpr int A_BYTES = BM * BK * 4;                  // 8 KB
 constexpr int B_BYTES = BNH * BK * 4;                 // 8 KB
 constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
-constexpr int EPI_WARPS = 8;
-constexpr int COLS_W = BN / 2;  // columns per epilogue warp
+#ifndef MT_TCF_EPI
+#define MT_TCF_EPI 8
+#endif
+constexpr int EPI_WARPS = MT_TCF_EPI;  // 8 or 16: 2 or 4 warps per TMEM lane quadrant
+static_assert(EPI_WARPS == 8 || EPI_WARPS == 16, "epilogue warps");
+constexpr int COLS_W = BN / (EPI_WARPS / 4);  // columns per epilogue warp
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 #ifndef MT_TCF_CSLOTS
 #define MT_TCF_CSLOTS (MT_TCF_BK == 32 ? 2 : 3)
@@ -399,7 +403,7 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
     // ------------------------------------------------ epilogue (warps 2..9, both CTAs)
     const int ew = warp - 2;
     const int q = warp & 3;     // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;   // column half of the item
+    const int half = ew >> 2;   // column part of the item (COLS_W wide)
     unsigned char* slots = epi + ew * CSLOTS * CSLOT_BYTES;
     uint64_t* wbar = cbar + ew * CSLOTS;
     const uint32_t tempty_l0 = peer_addr(&tempty[0], plead), tempty_l1 = peer_addr(&tempty[1], plead);
