@@ -75,6 +75,11 @@ constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
 constexpr int EPI_WARPS = MT_TCF_EPI;  // 8 or 16: 2 or 4 warps per TMEM lane quadrant
 static_assert(EPI_WARPS == 8 || EPI_WARPS == 16, "epilogue warps");
 constexpr int COLS_W = BN / (EPI_WARPS / 4);  // columns per epilogue warp
+#ifndef MT_TCF_LDX
+#define MT_TCF_LDX 16
+#endif
+constexpr int LDX = MT_TCF_LDX;  // TMEM columns per tcgen05.ld (+ wait::ld) in the drain
+static_assert(LDX == 16 || LDX == 32, "TMEM load width");
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 #ifndef MT_TCF_CSLOTS
 #define MT_TCF_CSLOTS (MT_TCF_BK == 32 ? 2 : 3)
@@ -142,6 +147,8 @@ __device__ __forceinline__ void ld16(uint32_t (&v)[16], uint32_t taddr) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void ldtm(uint32_t (&v)[16], uint32_t taddr) { ld16(v, taddr); }
+__device__ __forceinline__ void ldtm(uint32_t (&v)[32], uint32_t taddr) { ld32(v, taddr); }
 // 2-CTA TMA multicast (cta_group::2): the box lands at the same smem offset in
 // every CTA of `mask`; each destination's bytes complete on the `full` barrier
 // of that destination's pair leader (the peer bit of the barrier address
@@ -441,11 +448,11 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
         mbar_wait(&tfull[b], (ch >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-        for (int m = 0; m < COLS_W / 16; ++m) {
-          uint32_t v[16];
-          ld16(v, tq + b * BN + m * 16);
+        for (int m = 0; m < COLS_W / LDX; ++m) {
+          uint32_t v[LDX];
+          ldtm(v, tq + b * BN + m * LDX);
 #pragma unroll
-          for (int u = 0; u < 16; ++u) sum[16 * m + u] += __uint_as_float(v[u]);
+          for (int u = 0; u < LDX; ++u) sum[LDX * m + u] += __uint_as_float(v[u]);
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
