@@ -485,9 +485,8 @@ def run_ours(args, rank, world, local_rank):
         "share_of_step": d["ms"] / (t_dev / args.steps * 1e3),
         "traffic_source": (f"profiles/ncu_traffic.json: ncu dram__bytes_read+write per bulk-update "
                            f"launch ({dom_kernel}, one evaluation at the bench config); above "
-                           "the algorithmic C read+write because the A-panel rows are re-fetched "
-                           "per output column (the panel, 2 MB/tile, exceeds L2); ~45% of HBM "
-                           "bandwidth (DESIGN.md section 4)"),
+                           "the algorithmic C read+write because the A-panel row tiles are re-fetched "
+                           "once per super-column of 12 output columns (DESIGN.md section 4)"),
         "cholesky_flop_weighted": {
             "roofline_ms": t_roof * 1e3, "achieved_ms": t_chol * 1e3, "frac": t_roof / t_chol,
             "f_sp": fl_plan.sp, "f_dp": fl_plan.dp,

@@ -301,7 +301,7 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   4: CTAs of the lookahead panel-column FP32 update (0 = all SMs)
  *   5: SMs the bulk FP32 update yields to the panel kernels on request (0 = off)
  *   6: super-column width (owned tile columns) of the bulk FP32 update's output
- *      order, for L2 reuse of the panel operands (default 8; 0 = column-by-column
+ *      order, for L2 reuse of the panel operands (default 12; 0 = column-by-column
  *      slot order; single process row only)
  *   7, 8, 9: retired (round-1 single-CTA tcgen05 kernel A/B switches; -1)
  *  10: 1 = co-schedule the FP64 band update (programmatic dependent launch) on the

@@ -292,7 +292,7 @@ static int g_legacy_dmma = 0;  // 1 = register-staged DMMA band update (A/B comp
 static int g_pcol_ctas = 64;   // CTAs of the lookahead panel-column FP32 update (0 = all SMs)
 static int g_yield_sms = 32;   // SMs the bulk update yields to the panel TRSM (0 = off)
 static int g_tc_trsm = 1;      // 1 = off-band TRSM as a tcgen05 3xTF32 GEMM against L_kk^{-1}
-static int g_super_cols = 8;   // super-column width of the bulk FP32 update order (0 = slot order)
+static int g_super_cols = 12;  // super-column width of the bulk FP32 update order (0 = slot order)
 static int g_coschedule = 1;   // 1 = band DMMA update co-scheduled beside the capped FP32 update
 static int g_cosched_pct = 90; // band update's SM share, % of its work share (option 11)
 static int g_wide_items = 1;   // 1 = bulk FP32 update on 256 x 512 pair items (nb % 512 == 0)
