@@ -14,6 +14,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --clock-control none -k regex:tcf_update_kernel -c 1100 --csv --log-file $out/traffic_${tag}_tcf.csv \
   python tools/prof_eval.py --n 262144 --t 8 --warm 0 --reps 1 > /dev/null 2>&1
 echo traffic_rc=$?
-MT_OPTS=10=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tcf_update_kernel -s 20 -c 1 \
+MT_OPTS=10=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tcf_update_kernel -s 81 -c 1 \
   -o $out/full_${tag}_tcf python tools/prof_eval.py --n 65536 --t 8 --warm 0 --reps 1 > /dev/null 2>&1
 echo full_rc=$?
