@@ -75,6 +75,9 @@ constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // hi + lo = 32 KB
 constexpr int EPI_WARPS = MT_TCF_EPI;  // 8 or 16: 2 or 4 warps per TMEM lane quadrant
 static_assert(EPI_WARPS == 8 || EPI_WARPS == 16, "epilogue warps");
 constexpr int COLS_W = BN / (EPI_WARPS / 4);  // columns per epilogue warp
+#ifndef MT_TCF_RED_PREFETCH
+#define MT_TCF_RED_PREFETCH 1  // reduce-add epilogue: prefetch the item's C into L2 at its start
+#endif
 #ifndef MT_TCF_LDX
 #define MT_TCF_LDX 16
 #endif
@@ -462,7 +465,8 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           // C of this item: slots free once the previous item's stores were read
           if (out == OUT_UPDATE && w.red) {
             // the reduce-adds at the end of the item find C in L2
-            for (int m = 0; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
+            if (MT_TCF_RED_PREFETCH)
+              for (int m = 0; m < NCW; ++m) prefetch_l2_2d(&map_c, n0 + m * CW, crow);
           } else if (out == OUT_UPDATE) {
             bulk_wait_read<0>();
             for (int m = 0; m < CSLOTS; ++m) load_c(m, n0 + m * CW, crow);
