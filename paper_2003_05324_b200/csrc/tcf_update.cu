@@ -82,6 +82,9 @@ constexpr int COLS_W = BN / (EPI_WARPS / 4);  // columns per epilogue warp
 // (no prefetch: 1.1% faster at N=262144, DRAM 112.9 -> 111.8 GB per launch)
 #define MT_TCF_RED_PREFETCH 0
 #endif
+#ifndef MT_TCF_L2HINT
+#define MT_TCF_L2HINT 0  // 1 = B slabs evict_last, C reduce-adds evict_first (A/B)
+#endif
 #ifndef MT_TCF_LDX
 #define MT_TCF_LDX 16
 #endif
@@ -351,6 +354,11 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
             tma_load_pair_mc(sb + A_BYTES + boff, &map_b, &full[st], bmask, ks * BK, brow);
             tma_load_pair_mc(sb + 2 * A_BYTES + B_BYTES + boff, &map_b, &full[st], bmask, ks * BK,
                              brow + nb);
+          } else if (MT_TCF_L2HINT && !TRSM) {
+            // column operands stay in L2 for the whole super-column
+            const uint64_t pol = l2_policy_evict_last();
+            tma_load_pair_hint(sb + A_BYTES, &map_b, bar, ks * BK, brow, pol);
+            tma_load_pair_hint(sb + 2 * A_BYTES + B_BYTES, &map_b, bar, ks * BK, brow + nb, pol);
           } else {
             tma_load_pair(sb + A_BYTES, &map_b, bar, ks * BK, brow);                     // B hi
             tma_load_pair(sb + 2 * A_BYTES + B_BYTES, &map_b, bar, ks * BK, brow + nb);  // B lo
@@ -519,7 +527,11 @@ __device__ __forceinline__ void tcf_body(const Grid& g, int k, const WorkF& w,
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_reduce_add_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * CW, crow);
+            if (MT_TCF_L2HINT)  // C is not read again in this step
+              tma_reduce_add_2d_hint(&map_c, slots + s * CSLOT_BYTES, n0 + m * CW, crow,
+                                     l2_policy_evict_first());
+            else
+              tma_reduce_add_2d(&map_c, slots + s * CSLOT_BYTES, n0 + m * CW, crow);
             bulk_commit();
           }
         }
