@@ -299,7 +299,8 @@ int mt_peak_probe(int32_t kind, int32_t iters, double* tflops);
  *   3: off-band panel TRSM: 1 = tcgen05 3xTF32 GEMM against L_kk^{-1} (default),
  *      0 = SIMT blocked substitution against 32x32 diagonal-block inverses
  *   4: CTAs of the lookahead panel-column FP32 update (0 = all SMs)
- *   5: SMs the bulk FP32 update yields to the panel kernels on request (0 = off)
+ *   5: SMs the bulk FP32 update yields to the panel kernels on request (default 0 =
+ *      off on one GPU, where the panel chain is hidden; the P x Q path asks for 32)
  *   6: super-column width (owned tile columns) of the bulk FP32 update's output
  *      order, for L2 reuse of the panel operands (default 12; 0 = column-by-column
  *      slot order; single process row only)

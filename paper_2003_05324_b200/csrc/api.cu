@@ -290,7 +290,7 @@ static int g_engine = MT_ENGINE_TF32X3;
 static int g_update_ctas = 0;  // 0 = all SMs
 static int g_legacy_dmma = 0;  // 1 = register-staged DMMA band update (A/B comparisons)
 static int g_pcol_ctas = 64;   // CTAs of the lookahead panel-column FP32 update (0 = all SMs)
-static int g_yield_sms = 32;   // SMs the bulk update yields to the panel TRSM (0 = off)
+static int g_yield_sms = 0;    // SMs the bulk update yields to the panel TRSM (0 = off: at g = 1 the panel chain is hidden, yielding cost 0.4%)
 static int g_tc_trsm = 1;      // 1 = off-band TRSM as a tcgen05 3xTF32 GEMM against L_kk^{-1}
 static int g_super_cols = 12;  // super-column width of the bulk FP32 update order (0 = slot order)
 static int g_coschedule = 1;   // 1 = band DMMA update co-scheduled beside the capped FP32 update
